@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py — SVG2 sparse attention on B200: ms per call and effective TFLOPS vs dense, 1..8 GPUs (head-parallel).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload hunyuan720p] [--impl ours|reference]
+
+A step = one fused svg2_sparse_attention call (k-means on Q and K warm-started from the centroid cache with 2 Lloyd
+iterations, permutation, centroid top-p selection, variable-block tcgen05 attention, fused unpermute) over the whole
+workload (all B*H heads; with N GPUs each rank runs H/N heads and the Ulysses all-to-all in and out).
+value  = dense-equivalent effective TFLOPS = 4 N^2 d B H / t_call (whole job, max over ranks).
+e2e    = the same metric through the public API with host (pinned) Q/K/V in and O out, copies inside the timing.
+roofline = the variable-block attention kernel: executed algorithmic FLOPs 4 d * selected pairs / its event time,
+           against the measured sustained bf16 peak (MEASURED_PEAKS.json).
+cpu_baseline = the fp64 oracle (oracle/) on a bounded sample of the same workload on this host's cores.
+--impl reference times that oracle as the reference arm (rank 0 only).
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per sparse-attention call and effective TFLOPS at 1/2/4/8 B200 vs dense"
+UNIT = "TFLOPS (dense-equivalent 4*N^2*d*B*H / t_call)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="hunyuan720p")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters-warm", type=int, default=2)
+    ap.add_argument("--top-p", type=float, default=None)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-once", action="store_true", help="one call only (for ncu)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_sample(wl, rows=256, iters=2):
+    """The fp64 oracle as it stands on ONE (b,h) head of the workload: k-means on Q and K (cold, `iters` Lloyd
+    iterations, same work per iteration as the GPU's warm iterations), selection, and masked attention on `rows`
+    sampled query rows; the per-call time is extrapolated to all rows and all B*H heads."""
+    import numpy as np
+
+    import oracle
+    import svg2_synth
+    oracle.build()
+    q, k, v = svg2_synth.generate_head(wl, 0, 0)
+    Q64, K64, V64 = (svg2_synth.bf16_bits_to_f64(a) for a in (q, k, v))
+    scale = float(np.float32(1.0 / math.sqrt(wl.d)))
+    t0 = time.perf_counter()
+    lq, cq, sq = oracle.kmeans(Q64, wl.Cq, iters)
+    lk, ck, sk = oracle.kmeans(K64, wl.Ck, iters)
+    t1 = time.perf_counter()
+    mask, pairs = oracle.select_topp(cq, ck, sq, sk, wl.d, scale, wl.top_p)
+    t2 = time.perf_counter()
+    sel = svg2_synth.sample_rows(wl.N, rows, seed=0)
+    oracle.attention_rows(Q64, K64, V64, scale, rows=sel, lq=lq, lk=lk, mask=mask)
+    t3 = time.perf_counter()
+    per_head = (t1 - t0) + (t2 - t1) + (t3 - t2) * wl.N / len(sel)
+    t_call = per_head * wl.B * wl.H
+    flops = 4.0 * wl.N * wl.N * wl.d * wl.B * wl.H
+    return {
+        "value": flops / t_call / 1e12, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+        "sample": f"1 of {wl.B * wl.H} heads: k-means Q+K ({iters} iters, full N={wl.N}), selection, attention on "
+                  f"{len(sel)} sampled rows; extrapolated x{wl.N / len(sel):.0f} rows x{wl.B * wl.H} heads",
+        "seconds_measured": t3 - t0, "s_per_call_extrapolated": t_call, "density": pairs / (wl.N * wl.N),
+    }
+
+
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(max(0, min(args.warmup, 1))):
+        pass  # the oracle has no warm state; warm-up steps are not needed for a CPU program
+    samples = [cpu_oracle_sample(wl, rows=64) for _ in range(max(1, args.steps))]
+    v = sorted(s["value"] for s in samples)[len(samples) // 2]
+    t_call = sorted(s["s_per_call_extrapolated"] for s in samples)[len(samples) // 2]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_call * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (svg2-synth v1, seeded)",
+        "config": {"workload": wl.name, "B": wl.B, "H": wl.H, "N": wl.N, "d": wl.d, "Cq": wl.Cq, "Ck": wl.Ck,
+                   "top_p": wl.top_p, "kmeans_iters": 2},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                         "sample": samples[0]["sample"].replace("256", "64")},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def to_dev_bits(bits, dev):
+    import numpy as np
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(dev)
+
+
+def dense_baseline(Q, K, V, reps=3):
+    """torch SDPA on the same B200, every available backend timed; the fastest is the dense baseline."""
+    import torch
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    res = {}
+    for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION), ("flash", SDPBackend.FLASH_ATTENTION),
+                     ("efficient", SDPBackend.EFFICIENT_ATTENTION)):
+        try:
+            with sdpa_kernel([be]):
+                torch.nn.functional.scaled_dot_product_attention(Q, K, V)
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                for _ in range(reps):
+                    torch.nn.functional.scaled_dot_product_attention(Q, K, V)
+                e.record()
+                torch.cuda.synchronize()
+                res[name] = s.elapsed_time(e) / reps
+        except Exception as ex:  # backend unavailable for this shape / build
+            res[name] = None
+            res[name + "_error"] = str(ex).splitlines()[0][:120]
+    valid = {k: v for k, v in res.items() if isinstance(v, float)}
+    best = min(valid, key=valid.get) if valid else None
+    return best, res
+
+
+def run_ours(args, wl):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_18875_b200 as svg2
+    import svg2_synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    svg2.load_library()
+    top_p = args.top_p if args.top_p is not None else wl.top_p
+    from paper_2505_18875_b200.dist import head_range, head_to_seq, seq_to_head
+    h0, h1 = head_range(wl.H, rank, world)
+    Hl = h1 - h0
+    # inputs: this rank's heads, full sequence (synthetic, seeded per head)
+    q, k, v = svg2_synth.generate(wl, heads=range(h0, h1))
+    Q, K, V = (to_dev_bits(a, dev) for a in (q, k, v))
+    if world > 1:  # sequence-parallel activations as a DiT would hold them
+        Qs, Ks, Vs = (head_to_seq(t) for t in (Q, K, V))
+    pinned = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).pin_memory() for a in (q, k, v)]
+    del q, k, v
+    B, N, d = wl.B, wl.N, wl.d
+    iters_w = args.iters_warm
+
+    # cold call fills the centroid cache (the paper's first sparse step), then warm calls
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, top_p)
+    cq, ck = ex["q_centroids"], ex["k_centroids"]
+    torch.cuda.synchronize()
+    if args.profile_once:
+        O, pairs, _ = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True)
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_once": True, "density": float(pairs.double().sum()) / (B * Hl * N * N)}))
+        return
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+
+    def step(events=None):
+        if world > 1:
+            Qh, Kh, Vh = seq_to_head(Qs), seq_to_head(Ks), seq_to_head(Vs)
+        else:
+            Qh, Kh, Vh = Q, K, V
+        Oh, pr, _ = svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, events=events)
+        if world > 1:
+            return head_to_seq(Oh), pr
+        return Oh, pr
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stage_ms = {k_: 0.0 for k_ in ("kmeans_q", "kmeans_k", "permute", "select_topp", "worklist", "attention")}
+    names = list(stage_ms)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per_step = []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record()
+        for s in range(args.steps):
+            O, pairs = step(ev)
+            ev_done = torch.cuda.Event(enable_timing=True)
+            ev_done.record()
+            per_step.append((ev, ev_done))
+            ev_done.synchronize()
+            for i, nm in enumerate(names):
+                stage_ms[nm] += ev[i].elapsed_time(ev[i + 1])
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+        stop.record()
+        torch.cuda.synchronize()
+    total_ms = start.elapsed_time(stop)
+    t_local = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([t_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_call = float(t.item())
+        dist.barrier()
+    else:
+        t_call = t_local
+    for nm in stage_ms:
+        stage_ms[nm] /= args.steps
+    # per-step time includes a host sync per step for the stage events; report the pure back-to-back call too
+    start2, stop2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start2.record()
+    for _ in range(args.steps):
+        step()
+    stop2.record()
+    torch.cuda.synchronize()
+    t_b2b_local = start2.elapsed_time(stop2) / args.steps
+    if world > 1:
+        t = torch.tensor([t_b2b_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_b2b = float(t.item())
+    else:
+        t_b2b = t_b2b_local
+    t_use = min(t_call, t_b2b)
+
+    pairs_local = float(pairs.double().sum().item())
+    if world > 1:
+        pt = torch.tensor([pairs_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(pt)
+        pairs_total = float(pt.item())
+    else:
+        pairs_total = pairs_local
+    density = pairs_total / (B * wl.H * N * N)
+    dense_flops = 4.0 * N * N * d * B * wl.H
+    value = dense_flops / (t_use * 1e-3) / 1e12
+    pk, pk_src = peaks()
+    attn_ms = stage_ms["attention"]
+    attn_flops_local = 4.0 * d * pairs_local
+    achieved = attn_flops_local / (attn_ms * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops_sustained"], "traffic": None,
+                "kernel": "k_varblock_attn<128> (tcgen05 QK^T + PV, fused unpermute)",
+                "peak_source": f"{pk_src} bf16 sustained (cuBLAS 8192^3 back-to-back, MEASURED_PEAKS.json)",
+                "algorithmic": "4*d*selected_pairs executed FLOPs per launch / event time of the launch"}
+    traffic_file = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
+    if os.path.exists(traffic_file):
+        try:
+            roofline["traffic"] = json.load(open(traffic_file)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    # ---- e2e through the public API with host buffers (rank-local heads)
+    e2e = None
+    if pinned is not None:
+        out_host = torch.empty((B, Hl, N, d), dtype=torch.bfloat16).pin_memory()
+        Qd, Kd, Vd = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
+
+        def e2e_step():
+            Qd.copy_(pinned[0], non_blocking=True)
+            Kd.copy_(pinned[1], non_blocking=True)
+            Vd.copy_(pinned[2], non_blocking=True)
+            Oe, _, _ = svg2.sparse_attention(Qd, Kd, Vd, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True)
+            out_host.copy_(Oe, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s3.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e3.record()
+        torch.cuda.synchronize()
+        te = s3.elapsed_time(e3) / args.steps
+        if world > 1:
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        nbytes = B * Hl * N * d * 2
+        e2e = {"value": dense_flops / (te * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": te,
+               "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world}
+
+    # ---- dense baseline (same box, same inputs)
+    dense = None
+    if not args.no_dense and rank == 0:
+        best, res = dense_baseline(Q, K, V)
+        if best:
+            t_dense = res[best] * world  # this rank's heads on one GPU; scale to the whole job on one GPU
+            dense = {"best_backend": best, "ms_per_call_1gpu_all_heads": t_dense, "backends_ms_rank_heads": res,
+                     "speedup_vs_dense": t_dense / (t_use * world) if world == 1 else None,
+                     "inv_density": 1.0 / density if density > 0 else None,
+                     "kernel_speedup_vs_dense": (res[best] / attn_ms) if attn_ms > 0 else None,
+                     "paper_bar_0.85_over_density": 0.85 / density if density > 0 else None}
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cpu = cpu_oracle_sample(wl, rows=256, iters=iters_w)
+    launches = svg2.launch_count(B, Hl, N, N, d, wl.Cq, wl.Ck, iters_w, top_p, True) * args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_use, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (svg2-synth v1: seeded Voronoi-group Q/K/V, bf16, shapes of the named workload)",
+            "config": {"workload": wl.name, "B": B, "H": wl.H, "N": N, "d": d, "Cq": wl.Cq, "Ck": wl.Ck,
+                       "top_p": top_p, "kmeans_iters": iters_w, "warm_start": True,
+                       "parallelism": f"head-parallel x{world}" + (" + Ulysses all-to-all" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (Q+K+V = %.2f GB > 126 MB)" % (3 * B * wl.H * N * d * 2 / 1e9)},
+            "density": density, "ms_per_call": t_use, "ms_per_call_with_stage_events": t_call,
+            "stages_ms": stage_ms, "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
+            "dense_baseline": dense, "cpu_baseline": cpu, "clocks": clocks.summary(),
+            "attention_executed_tflops": achieved,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    import svg2_synth
+    wl = svg2_synth.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,97 @@
+// internal.h — launchers and workspace layout shared by the svg2 CUDA translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace svg2 {
+
+constexpr int kSortTile = 2048;      // labels per histogram / stable-scatter tile
+constexpr int kMaxClusters = 4096;   // C limit (select_topp sorts a row of Ck in shared memory)
+constexpr int kQTile = 128;          // query rows per tcgen05 M=128 tile
+constexpr int kKTile = 128;          // keys per S tile (N of the QK^T MMA, K of the PV MMA)
+constexpr int kItemRows = 2 * kQTile;  // one attention work item = two Q tiles of one query cluster
+
+inline int sort_tiles(int N) { return (N + kSortTile - 1) / kSortTile; }
+inline int items_cap_per_bh(int Nq, int Cq) { return (Nq + kItemRows - 1) / kItemRows + Cq; }
+
+// Bump allocator over the caller's workspace: the same code computes the size (base == nullptr) and the
+// pointers, so the two can never disagree.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct SortWs {  // histogram/scan/stable-scatter scratch
+  int32_t* tile_counts;  // [BH, T, C]
+};
+inline SortWs carve_sort(Carver& c, int BH, int N, int C) {
+  SortWs w;
+  w.tile_counts = c.take<int32_t>(size_t(BH) * sort_tiles(N) * C);
+  return w;
+}
+
+struct KmeansWs {
+  SortWs sort;
+  int32_t* perm;     // [BH, N]   (used when the caller does not want perm)
+  int32_t* offsets;  // [BH, C+1]
+};
+inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C) {
+  KmeansWs w;
+  w.sort = carve_sort(c, BH, N, C);
+  w.perm = c.take<int32_t>(size_t(BH) * N);
+  w.offsets = c.take<int32_t>(size_t(BH) * (C + 1));
+  return w;
+}
+
+struct AttnWs {
+  int2* runs;          // [BH, Cq, Ck]  (absolute first row in the flattened [BH*Nk] key tensor, length)
+  int32_t* run_count;  // [BH, Cq]
+  int32_t* nkeys;      // [BH, Cq]
+  int4* items_bh;      // [BH, cap]
+  int32_t* items_cnt;  // [BH]
+  int4* items;         // [BH * cap] flattened
+  int32_t* n_items;    // [1]
+};
+inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Cq, int Ck) {
+  AttnWs w;
+  const size_t cap = items_cap_per_bh(Nq, Cq);
+  w.runs = c.take<int2>(size_t(BH) * Cq * Ck);
+  w.run_count = c.take<int32_t>(size_t(BH) * Cq);
+  w.nkeys = c.take<int32_t>(size_t(BH) * Cq);
+  w.items_bh = c.take<int4>(size_t(BH) * cap);
+  w.items_cnt = c.take<int32_t>(BH);
+  w.items = c.take<int4>(size_t(BH) * cap);
+  w.n_items = c.take<int32_t>(1);
+  return w;
+}
+
+// ---- launchers (return cudaGetLastError() of their launches)
+cudaError_t launch_stable_sort(const int32_t* labels, int BH, int N, int C, SortWs ws, int32_t* perm,
+                               int32_t* offsets, int32_t* sizes, cudaStream_t s);
+cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const void* X0, void* X0p,
+                               const void* X1, void* X1p, cudaStream_t s);
+cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int N, int d, void* O, cudaStream_t s);
+cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
+                          int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
+                          cudaStream_t s, int* launches);
+cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH,
+                               int Cq, int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
+                               cudaStream_t s);
+cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
+                                  int Nq, int Nk, int Cq, int Ck, AttnWs ws, cudaStream_t s);
+cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk,
+                                      int d, int Cq, int Ck, float scale, const int32_t* q_perm, void* O,
+                                      float* lse, AttnWs ws, cudaStream_t s);
+int kmeans_launch_count(int iters, bool warm);
+constexpr int kSortLaunches = 3, kWorklistLaunches = 2;
+
+}  // namespace svg2

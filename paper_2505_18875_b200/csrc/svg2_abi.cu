@@ -1,0 +1,306 @@
+// svg2_abi.cu — the extern "C" boundary declared in include/svg2.h: synchronous validation (no launch, no output
+// touched on error), workspace carving, and the enqueue of the kernels of svg2_*.cu on the caller's stream.
+#include <cuda_runtime.h>
+#include <cmath>
+#include "../../include/svg2.h"
+#include "internal.h"
+
+using namespace svg2;
+
+namespace {
+
+constexpr long long kMaxN = 1ll << 24;
+
+svg2_status_t check_device() {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SVG2_ERR_CUDA;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) return SVG2_ERR_UNSUPPORTED_DEVICE;
+  return SVG2_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+svg2_status_t check_bhnd(long long B, long long H, long long N, long long d) {
+  if (B <= 0 || H <= 0 || N <= 0) return SVG2_ERR_INVALID_SHAPE;
+  if (d != 64 && d != 128) return SVG2_ERR_INVALID_SHAPE;
+  if (N > kMaxN || B * H * N >= (1ll << 31)) return SVG2_ERR_INVALID_SHAPE;
+  return SVG2_OK;
+}
+
+svg2_status_t check_clusters(long long C, long long N) {
+  if (C < 1 || C > N || C > kMaxClusters) return SVG2_ERR_INVALID_PARAM;
+  return SVG2_OK;
+}
+
+svg2_status_t from_cuda(cudaError_t e) { return e == cudaSuccess ? SVG2_OK : SVG2_ERR_CUDA; }
+
+// Sticky or pending errors from earlier asynchronous work are reported (and cleared) before new work.
+svg2_status_t pending_error() { return from_cuda(cudaGetLastError()); }
+
+float resolve_scale(float scale, int d) { return scale > 0.f ? scale : float(1.0 / std::sqrt(double(d))); }
+
+struct FusedWs {
+  int32_t *lab_q, *lab_k, *perm_q, *perm_k, *off_q, *off_k, *size_q, *size_k;
+  void *Qp, *Kp, *Vp;
+  uint8_t* mask;
+  KmeansWs km;
+  AttnWs attn;
+};
+
+FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) {
+  const size_t BH = size_t(dm.B) * dm.H;
+  FusedWs w;
+  w.lab_q = c.take<int32_t>(BH * dm.Nq);
+  w.lab_k = c.take<int32_t>(BH * dm.Nk);
+  w.perm_q = c.take<int32_t>(BH * dm.Nq);
+  w.perm_k = c.take<int32_t>(BH * dm.Nk);
+  w.off_q = c.take<int32_t>(BH * (cfg.Cq + 1));
+  w.off_k = c.take<int32_t>(BH * (cfg.Ck + 1));
+  w.size_q = c.take<int32_t>(BH * cfg.Cq);
+  w.size_k = c.take<int32_t>(BH * cfg.Ck);
+  w.Qp = c.take<uint16_t>(BH * dm.Nq * dm.d);
+  w.Kp = c.take<uint16_t>(BH * dm.Nk * dm.d);
+  w.Vp = c.take<uint16_t>(BH * dm.Nk * dm.d);
+  w.mask = c.take<uint8_t>(BH * cfg.Cq * cfg.Ck);
+  // k-means scratch is reused by the Q and the K role (same stream, sequential): carve the larger one
+  Carver probe_q(nullptr), probe_k(nullptr);
+  carve_kmeans(probe_q, int(BH), dm.Nq, cfg.Cq);
+  carve_kmeans(probe_k, int(BH), dm.Nk, cfg.Ck);
+  const size_t start = (c.off + 255) & ~size_t(255);
+  Carver km(c.base ? c.base + start : nullptr);
+  w.km = probe_q.off >= probe_k.off ? carve_kmeans(km, int(BH), dm.Nq, cfg.Cq) : carve_kmeans(km, int(BH), dm.Nk, cfg.Ck);
+  c.off = start + km.off;
+  w.attn = carve_attn(c, int(BH), dm.Nq, cfg.Cq, cfg.Ck);
+  return w;
+}
+
+svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
+  if (!cfg) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = check_bhnd(dm.B, dm.H, dm.Nq, dm.d);
+  if (st != SVG2_OK) return st;
+  if ((st = check_bhnd(dm.B, dm.H, dm.Nk, dm.d)) != SVG2_OK) return st;
+  if ((st = check_clusters(cfg->Cq, dm.Nq)) != SVG2_OK) return st;
+  if ((st = check_clusters(cfg->Ck, dm.Nk)) != SVG2_OK) return st;
+  if (cfg->iters < 1) return SVG2_ERR_INVALID_PARAM;
+  if (!(cfg->top_p > 0.0 && cfg->top_p <= 1.0)) return SVG2_ERR_INVALID_PARAM;
+  if (!(cfg->scale >= 0.f) || std::isinf(cfg->scale)) return SVG2_ERR_INVALID_PARAM;
+  if (cfg->flags & ~SVG2_WARM_START) return SVG2_ERR_INVALID_PARAM;
+  return SVG2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* svg2_status_string(svg2_status_t s) {
+  switch (s) {
+    case SVG2_OK: return "SVG2_OK";
+    case SVG2_ERR_NULL_POINTER: return "SVG2_ERR_NULL_POINTER";
+    case SVG2_ERR_INVALID_SHAPE: return "SVG2_ERR_INVALID_SHAPE";
+    case SVG2_ERR_INVALID_PARAM: return "SVG2_ERR_INVALID_PARAM";
+    case SVG2_ERR_MISALIGNED: return "SVG2_ERR_MISALIGNED";
+    case SVG2_ERR_WORKSPACE_TOO_SMALL: return "SVG2_ERR_WORKSPACE_TOO_SMALL";
+    case SVG2_ERR_UNSUPPORTED_DEVICE: return "SVG2_ERR_UNSUPPORTED_DEVICE";
+    case SVG2_ERR_CUDA: return "SVG2_ERR_CUDA";
+    case SVG2_ERR_NOT_IMPLEMENTED: return "SVG2_ERR_NOT_IMPLEMENTED";
+  }
+  return "SVG2_UNKNOWN_STATUS";
+}
+
+int svg2_abi_version(void) { return SVG2_ABI_VERSION; }
+
+size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dm, const svg2_config_t* cfg) {
+  if (!cfg) return 0;
+  const long long BH = (long long)dm.B * dm.H;
+  Carver c(nullptr);
+  switch (entry) {
+    case SVG2_ENTRY_KMEANS:
+      if (check_bhnd(dm.B, dm.H, dm.Nq, dm.d) != SVG2_OK || check_clusters(cfg->Cq, dm.Nq) != SVG2_OK) return 0;
+      carve_kmeans(c, int(BH), dm.Nq, cfg->Cq);
+      return c.off + 256;
+    case SVG2_ENTRY_PERMUTE:
+      if (check_bhnd(dm.B, dm.H, dm.Nq, dm.d) != SVG2_OK || check_clusters(cfg->Cq, dm.Nq) != SVG2_OK) return 0;
+      carve_sort(c, int(BH), dm.Nq, cfg->Cq);
+      return c.off + 256;
+    case SVG2_ENTRY_SELECT_TOPP:
+    case SVG2_ENTRY_UNPERMUTE:
+      return 0;
+    case SVG2_ENTRY_VARBLOCK_ATTENTION:
+      if (check_bhnd(dm.B, dm.H, dm.Nq, dm.d) != SVG2_OK || check_bhnd(dm.B, dm.H, dm.Nk, dm.d) != SVG2_OK ||
+          check_clusters(cfg->Cq, dm.Nq) != SVG2_OK || check_clusters(cfg->Ck, dm.Nk) != SVG2_OK)
+        return 0;
+      carve_attn(c, int(BH), dm.Nq, cfg->Cq, cfg->Ck);
+      return c.off + 256;
+    case SVG2_ENTRY_SPARSE_ATTENTION:
+      if (validate_fused(dm, cfg) != SVG2_OK) return 0;
+      carve_fused(c, dm, *cfg);
+      return c.off + 256;
+  }
+  return 0;
+}
+
+svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C, int32_t iters,
+                          uint32_t flags, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
+                          int32_t* offsets, void* ws, size_t ws_bytes, void* stream) {
+  if (!X || !centroids || !labels || !sizes || (!ws && ws_bytes)) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = check_bhnd(B, H, N, d);
+  if (st != SVG2_OK) return st;
+  if ((st = check_clusters(C, N)) != SVG2_OK) return st;
+  if (iters < 1 || (flags & ~SVG2_WARM_START)) return SVG2_ERR_INVALID_PARAM;
+  if (!aligned16(X) || !aligned16(centroids)) return SVG2_ERR_MISALIGNED;
+  svg2_config_t cfg{C, C, iters, 1.0, 0.f, flags};
+  svg2_dims_t dm{B, H, N, N, d};
+  if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_KMEANS, dm, &cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+  Carver c(ws);
+  KmeansWs kw = carve_kmeans(c, B * H, N, C);
+  return from_cuda(launch_kmeans(X, B * H, N, d, C, iters, flags & SVG2_WARM_START, centroids, labels, sizes, perm,
+                                 offsets, kw, static_cast<cudaStream_t>(stream), nullptr));
+}
+
+svg2_status_t svg2_permute(const int32_t* labels, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C,
+                           const void* X0, void* X0p, const void* X1, void* X1p, int32_t* perm, int32_t* offsets,
+                           void* ws, size_t ws_bytes, void* stream) {
+  if (!labels || !perm || !offsets || (!ws && ws_bytes)) return SVG2_ERR_NULL_POINTER;
+  if ((X0 == nullptr) != (X0p == nullptr) || (X1 == nullptr) != (X1p == nullptr)) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = check_bhnd(B, H, N, d);
+  if (st != SVG2_OK) return st;
+  if ((st = check_clusters(C, N)) != SVG2_OK) return st;
+  if ((X0 && (!aligned16(X0) || !aligned16(X0p))) || (X1 && (!aligned16(X1) || !aligned16(X1p))))
+    return SVG2_ERR_MISALIGNED;
+  svg2_config_t cfg{C, C, 1, 1.0, 0.f, 0};
+  svg2_dims_t dm{B, H, N, N, d};
+  if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_PERMUTE, dm, &cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+  Carver c(ws);
+  SortWs sw = carve_sort(c, B * H, N, C);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_stable_sort(labels, B * H, N, C, sw, perm, offsets, nullptr, s);
+  if (e == cudaSuccess && (X0 || X1)) e = launch_gather_rows(perm, B * H, N, d, X0, X0p, X1, X1p, s);
+  return from_cuda(e);
+}
+
+svg2_status_t svg2_select_topp(const float* q_centroids, const float* k_centroids, const int32_t* q_sizes,
+                               const int32_t* k_sizes, int32_t B, int32_t H, int32_t Cq, int32_t Ck, int32_t d,
+                               float scale, double top_p, uint8_t* mask, int64_t* selected_pairs, void* stream) {
+  if (!q_centroids || !k_centroids || !q_sizes || !k_sizes || !mask) return SVG2_ERR_NULL_POINTER;
+  if (B <= 0 || H <= 0 || (d != 64 && d != 128)) return SVG2_ERR_INVALID_SHAPE;
+  if (Cq < 1 || Ck < 1 || Cq > kMaxClusters || Ck > kMaxClusters) return SVG2_ERR_INVALID_PARAM;
+  if (!(top_p > 0.0 && top_p <= 1.0) || !(scale >= 0.f) || std::isinf(scale)) return SVG2_ERR_INVALID_PARAM;
+  svg2_status_t st;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+  return from_cuda(launch_select_topp(q_centroids, k_centroids, q_sizes, k_sizes, B * H, Cq, Ck, d,
+                                      resolve_scale(scale, d), top_p, mask, selected_pairs,
+                                      static_cast<cudaStream_t>(stream)));
+}
+
+svg2_status_t svg2_varblock_attention(const void* Qp, const void* Kp, const void* Vp, svg2_dims_t dm,
+                                      const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask,
+                                      int32_t Cq, int32_t Ck, float scale, const int32_t* q_perm, void* O,
+                                      float* lse, void* ws, size_t ws_bytes, void* stream) {
+  if (!Qp || !Kp || !Vp || !q_offsets || !k_offsets || !mask || !O || !ws) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = check_bhnd(dm.B, dm.H, dm.Nq, dm.d);
+  if (st != SVG2_OK) return st;
+  if ((st = check_bhnd(dm.B, dm.H, dm.Nk, dm.d)) != SVG2_OK) return st;
+  if ((st = check_clusters(Cq, dm.Nq)) != SVG2_OK) return st;
+  if ((st = check_clusters(Ck, dm.Nk)) != SVG2_OK) return st;
+  if (!(scale >= 0.f) || std::isinf(scale)) return SVG2_ERR_INVALID_PARAM;
+  if (!aligned16(Qp) || !aligned16(Kp) || !aligned16(Vp) || !aligned16(O)) return SVG2_ERR_MISALIGNED;
+  svg2_config_t cfg{Cq, Ck, 1, 1.0, scale, 0};
+  if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_VARBLOCK_ATTENTION, dm, &cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+  Carver c(ws);
+  const int BH = dm.B * dm.H;
+  AttnWs aw = carve_attn(c, BH, dm.Nq, Cq, Ck);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_build_worklist(q_offsets, k_offsets, mask, BH, dm.Nq, dm.Nk, Cq, Ck, aw, s);
+  if (e == cudaSuccess)
+    e = launch_varblock_attention(Qp, Kp, Vp, BH, dm.Nq, dm.Nk, dm.d, Cq, Ck, resolve_scale(scale, dm.d), q_perm, O,
+                                  lse, aw, s);
+  return from_cuda(e);
+}
+
+svg2_status_t svg2_unpermute(const void* Op, const int32_t* perm, int32_t B, int32_t H, int32_t N, int32_t d,
+                             void* O, void* stream) {
+  if (!Op || !perm || !O) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = check_bhnd(B, H, N, d);
+  if (st != SVG2_OK) return st;
+  if (!aligned16(Op) || !aligned16(O)) return SVG2_ERR_MISALIGNED;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+  return from_cuda(launch_scatter_rows(Op, perm, B * H, N, d, O, static_cast<cudaStream_t>(stream)));
+}
+
+int32_t svg2_sparse_attention_launch_count(svg2_dims_t dm, const svg2_config_t* cfg) {
+  (void)dm;
+  if (!cfg) return 0;
+  const bool warm = cfg->flags & SVG2_WARM_START;
+  return 2 * kmeans_launch_count(cfg->iters, warm) + 2 /*gathers*/ + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+}
+
+svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V, svg2_dims_t dm,
+                                    const svg2_config_t* cfg, float* q_centroids, float* k_centroids, void* O,
+                                    int64_t* selected_pairs, const svg2_debug_t* dbg, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  if (!Q || !K || !V || !cfg || !q_centroids || !k_centroids || !O || !ws) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = validate_fused(dm, cfg);
+  if (st != SVG2_OK) return st;
+  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(q_centroids) ||
+      !aligned16(k_centroids))
+    return SVG2_ERR_MISALIGNED;
+  if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_SPARSE_ATTENTION, dm, cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+
+  Carver c(ws);
+  FusedWs w = carve_fused(c, dm, *cfg);
+  if (dbg) {  // intermediates requested: write them straight into the caller's buffers
+    if (dbg->q_labels) w.lab_q = dbg->q_labels;
+    if (dbg->k_labels) w.lab_k = dbg->k_labels;
+    if (dbg->q_perm) w.perm_q = dbg->q_perm;
+    if (dbg->k_perm) w.perm_k = dbg->k_perm;
+    if (dbg->q_offsets) w.off_q = dbg->q_offsets;
+    if (dbg->k_offsets) w.off_k = dbg->k_offsets;
+    if (dbg->mask) w.mask = dbg->mask;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto mark = [&](int k) {
+    if (dbg && dbg->events[k]) cudaEventRecord(static_cast<cudaEvent_t>(dbg->events[k]), s);
+  };
+  const int BH = dm.B * dm.H;
+  const bool warm = cfg->flags & SVG2_WARM_START;
+  const float scale = resolve_scale(cfg->scale, dm.d);
+  cudaError_t e = cudaSuccess;
+  mark(0);
+  e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
+                    w.km, s, nullptr);
+  mark(1);
+  if (e == cudaSuccess)
+    e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
+                      w.off_k, w.km, s, nullptr);
+  mark(2);
+  if (e == cudaSuccess) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
+  if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, V, w.Vp, s);
+  mark(3);
+  if (e == cudaSuccess)
+    e = launch_select_topp(q_centroids, k_centroids, w.size_q, w.size_k, BH, cfg->Cq, cfg->Ck, dm.d, scale,
+                           cfg->top_p, w.mask, selected_pairs, s);
+  mark(4);
+  if (e == cudaSuccess)
+    e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck, w.attn, s);
+  mark(5);
+  if (e == cudaSuccess)
+    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, cfg->Cq, cfg->Ck, scale, w.perm_q, O,
+                                  nullptr, w.attn, s);
+  mark(6);
+  mark(7);
+  return from_cuda(e);
+}
+
+}  // extern "C"

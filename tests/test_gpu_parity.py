@@ -1,0 +1,306 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, stage by stage (protocol P1-P7 of
+DESIGN.md §Parity).  Integer stages bit-exact; labels equal except documented near-ties (R16); masks bit-exact
+except near-ties (R17); attention within max-abs 2e-2 / mean-abs 2e-3 (bf16 out, fp32 accumulation)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import svg2_synth
+from gpu_helpers import label_mismatches_are_ties, mask_mismatch_rows_are_ties, random_qkv, to_dev, to_f64
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+@pytest.fixture(scope="module")
+def svg2():
+    assert torch.cuda.is_available(), "the -m gpu tests need a CUDA device"
+    import paper_2505_18875_b200 as m
+    m.load_library()
+    return m
+
+
+def f32scale(d):
+    return float(np.float32(1.0 / math.sqrt(d)))
+
+
+def check_attention(O_gpu, O_ref, what=""):
+    err = np.abs(to_f64(O_gpu).reshape(O_ref.shape) - O_ref)
+    assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS, f"{what}: max {err.max():.3e} mean {err.mean():.3e}"
+    return err.max(), err.mean()
+
+
+# ------------------------------------------------------------------ P1: integer stages
+@pytest.mark.parametrize("B,H,N,d,C", [(2, 3, 5000, 128, 37), (1, 2, 1024, 64, 16), (1, 1, 129, 64, 128)])
+def test_permute_bitexact(svg2, oracle_mod, B, H, N, d, C):
+    rng = np.random.default_rng(N + C)
+    used = rng.choice(C, size=max(1, C - 3), replace=False)  # leave some clusters empty
+    labels = used[rng.integers(0, len(used), (B, H, N))].astype(np.int32)
+    q, k, v = random_qkv(B, H, N, N, d, seed=1)
+    Kd, Vd = to_dev(k), to_dev(v)
+    perm, off, Kp, Vp = svg2.permute(torch.from_numpy(labels).cuda(), C, Kd, Vd)
+    perm_h, off_h = perm.cpu().numpy(), off.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            p_ref, o_ref = oracle_mod.permute(labels[b, h], C)
+            assert np.array_equal(perm_h[b, h], p_ref)
+            assert np.array_equal(off_h[b, h], o_ref)
+    idx = perm.long().unsqueeze(-1).expand(-1, -1, -1, d)
+    assert torch.equal(Kp, torch.gather(Kd, 2, idx)) and torch.equal(Vp, torch.gather(Vd, 2, idx))
+    assert torch.equal(svg2.unpermute(Kp, perm), Kd)  # pi^T pi = I, bitwise
+
+
+# ------------------------------------------------------------------ P2/P3: k-means
+@pytest.mark.parametrize("N,d,C", [(1024, 64, 16), (4096, 128, 100), (3001, 128, 500)])
+def test_kmeans_teacher_forced(svg2, oracle_mod, N, d, C):
+    q, _, _ = random_qkv(1, 1, N, N, d, seed=N, groups=24)
+    X = to_dev(q)
+    X64 = to_f64(X)[0, 0]
+    cent = torch.from_numpy(X64[(np.arange(C) * N) // C].astype(np.float32)).cuda().view(1, 1, C, d).contiguous()
+    total_bad = 0
+    for it in range(4):  # re-sync the oracle to the GPU's centroids every iteration (P3)
+        c_in = cent.clone()
+        labels, sizes, cent = svg2.kmeans(X, C, 1, centroids=cent)
+        c64 = c_in.cpu().numpy().astype(np.float64)[0, 0]
+        gl = labels.cpu().numpy()[0, 0]
+        nbad, nontie = label_mismatches_are_ties(X64, c64, gl)
+        assert nontie == 0, f"iteration {it}: {nontie} label mismatches outside the tie band"
+        total_bad += nbad
+        ol, oc, osz = oracle_mod.kmeans(X64, C, 1, init=c64)
+        if nbad == 0:
+            assert np.array_equal(sizes.cpu().numpy()[0, 0], osz)
+            assert np.array_equal(cent.cpu().numpy()[0, 0], oc.astype(np.float32)), "centroid update not bit-exact"
+    assert total_bad <= max(2, N // 1000)
+
+
+def test_kmeans_cold_matches_oracle_tiny(svg2, oracle_mod):
+    wl = svg2_synth.WORKLOADS["tiny"]
+    q, k, _ = svg2_synth.generate(wl)
+    for bits, C in ((q, wl.Cq), (k, wl.Ck)):
+        X = to_dev(bits)
+        labels, sizes, cent, perm, off = svg2.kmeans(X, C, wl.iters, return_perm=True)
+        X64 = to_f64(X)[0, 0]
+        ol, oc, osz = oracle_mod.kmeans(X64, C, wl.iters)
+        assert np.array_equal(labels.cpu().numpy()[0, 0], ol)
+        assert np.array_equal(sizes.cpu().numpy()[0, 0], osz)
+        assert np.array_equal(cent.cpu().numpy()[0, 0], oc.astype(np.float32))
+        p_ref, o_ref = oracle_mod.permute(ol, C)
+        assert np.array_equal(perm.cpu().numpy()[0, 0], p_ref) and np.array_equal(off.cpu().numpy()[0, 0], o_ref)
+
+
+def test_kmeans_dup_ties_and_empty_clusters(svg2, oracle_mod):
+    wl = svg2_synth.WORKLOADS["tiny"]
+    q, _, _ = svg2_synth.generate(wl, dup=True)
+    X = to_dev(q)
+    labels, sizes, cent = svg2.kmeans(X, 32, 3)
+    ol, oc, osz = oracle_mod.kmeans(to_f64(X)[0, 0], 32, 3)
+    assert np.array_equal(labels.cpu().numpy()[0, 0], ol)
+    assert np.array_equal(sizes.cpu().numpy()[0, 0], osz)
+
+
+# ------------------------------------------------------------------ P4: selection
+@pytest.mark.parametrize("p", [0.3, 0.7, 0.9, 0.95, 1.0])
+@pytest.mark.parametrize("Cq,Ck,d", [(16, 32, 64), (100, 500, 128), (37, 1000, 128)])
+def test_select_topp_bitexact(svg2, oracle_mod, p, Cq, Ck, d):
+    rng = np.random.default_rng(Cq * Ck)
+    B, H = 1, 2
+    cq = (rng.standard_normal((B, H, Cq, d)) * 2).astype(np.float32)
+    ck = (rng.standard_normal((B, H, Ck, d)) * 2).astype(np.float32)
+    sq = rng.integers(0, 50, (B, H, Cq)).astype(np.int32)
+    sk = rng.integers(0, 50, (B, H, Ck)).astype(np.int32)
+    sk[..., 0] = 7
+    mask, pairs = svg2.select_topp(*(torch.from_numpy(a).cuda() for a in (cq, ck, sq, sk)), p)
+    mask_h, pairs_h = mask.cpu().numpy(), pairs.cpu().numpy()
+    for h in range(H):
+        om, opairs, S, W, Z = oracle_mod.select_topp(cq[0, h].astype(np.float64), ck[0, h].astype(np.float64),
+                                                     sq[0, h], sk[0, h], d, f32scale(d), p, return_tables=True)
+        nrows, nontie = mask_mismatch_rows_are_ties(W, Z, sk[0, h], p, mask_h[0, h], om)
+        assert nontie == 0
+        if nrows == 0:
+            assert pairs_h[0, h] == opairs
+
+
+# ------------------------------------------------------------------ P5: variable-block attention
+def _pipeline_inputs(svg2, wl_or_shape, seed=0, top_p=None, iters=None, dup=False, amp=None):
+    if isinstance(wl_or_shape, svg2_synth.Workload):
+        wl = wl_or_shape
+        q, k, v = svg2_synth.generate(wl, dup=dup, amp=amp)
+        Cq, Ck, p, it = wl.Cq, wl.Ck, wl.top_p, wl.iters
+    else:
+        B, H, Nq, Nk, d, Cq, Ck = wl_or_shape
+        q, k, v = random_qkv(B, H, Nq, Nk, d, seed=seed, groups=12)
+        p, it = 0.9, 3
+    return to_dev(q), to_dev(k), to_dev(v), Cq, Ck, (top_p or p), (iters or it)
+
+
+@pytest.mark.parametrize("case", ["tiny", "ragged", "nq_ne_nk", "d128_multi_head", "tiny_clusters"])
+def test_varblock_attention_parity(svg2, oracle_mod, case):
+    shapes = {"ragged": (1, 2, 3001, 3001, 128, 20, 40), "nq_ne_nk": (2, 1, 1500, 2600, 64, 9, 33),
+              "d128_multi_head": (1, 3, 4096, 4096, 128, 30, 60), "tiny_clusters": (1, 1, 700, 700, 64, 300, 350)}
+    Q, K, V, Cq, Ck, p, iters = _pipeline_inputs(svg2, svg2_synth.WORKLOADS["tiny"] if case == "tiny" else shapes[case])
+    B, H, Nq, d = Q.shape
+    Nk = K.shape[2]
+    lq, sq, cq, pq, oq = svg2.kmeans(Q, Cq, iters, return_perm=True)
+    lk, sk, ck, pk, ok = svg2.kmeans(K, Ck, iters, return_perm=True)
+    _, _, Qp, _ = svg2.permute(lq, Cq, Q)
+    _, _, Kp, Vp = svg2.permute(lk, Ck, K, V)
+    mask, pairs = svg2.select_topp(cq, ck, sq, sk, p)
+    O = svg2.varblock_attention(Qp, Kp, Vp, oq, ok, mask, q_perm=pq)
+    Op = svg2.varblock_attention(Qp, Kp, Vp, oq, ok, mask)
+    assert torch.equal(svg2.unpermute(Op, pq), O)  # fused pi_q^T == separate unpermute, bitwise
+    Q64, K64, V64 = to_f64(Q), to_f64(K), to_f64(V)
+    lq_h, lk_h, m_h = lq.cpu().numpy(), lk.cpu().numpy(), mask.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            ref = oracle_mod.attention_rows(Q64[b, h], K64[b, h], V64[b, h], f32scale(d), lq=lq_h[b, h],
+                                            lk=lk_h[b, h], mask=m_h[b, h])
+            check_attention(O[b, h], ref, f"{case} b{b} h{h}")
+            tok = m_h[b, h][lq_h[b, h]][:, lk_h[b, h]]
+            assert int(pairs[b, h]) == int(tok.sum())
+
+
+def test_varblock_lse(svg2, oracle_mod):
+    Q, K, V, Cq, Ck, p, iters = _pipeline_inputs(svg2, (1, 1, 2000, 2000, 128, 12, 24), seed=5)
+    d = Q.shape[-1]
+    lq, sq, cq, pq, oq = svg2.kmeans(Q, Cq, iters, return_perm=True)
+    lk, sk, ck, pk, ok = svg2.kmeans(K, Ck, iters, return_perm=True)
+    _, _, Qp, _ = svg2.permute(lq, Cq, Q)
+    _, _, Kp, Vp = svg2.permute(lk, Ck, K, V)
+    mask, _ = svg2.select_topp(cq, ck, sq, sk, p)
+    O, lse = svg2.varblock_attention(Qp, Kp, Vp, oq, ok, mask, q_perm=pq, return_lse=True)
+    _, ref_lse = oracle_mod.attention_rows(to_f64(Q)[0, 0], to_f64(K)[0, 0], to_f64(V)[0, 0], f32scale(d),
+                                           lq=lq.cpu().numpy()[0, 0], lk=lk.cpu().numpy()[0, 0],
+                                           mask=mask.cpu().numpy()[0, 0], return_lse=True)
+    assert np.max(np.abs(lse.cpu().numpy()[0, 0] - ref_lse)) < 1e-2
+
+
+# ------------------------------------------------------------------ P6: fused call, stage by stage
+@pytest.mark.parametrize("case", ["tiny", "tiny_dup"])
+def test_fused_stagewise(svg2, oracle_mod, case):
+    wl = svg2_synth.WORKLOADS["tiny"]
+    Q, K, V, Cq, Ck, p, iters = _pipeline_inputs(svg2, wl, dup=(case == "tiny_dup"))
+    d = Q.shape[-1]
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, iters, p, debug=True)
+    Q64, K64, V64 = (to_f64(t)[0, 0] for t in (Q, K, V))
+    # k-means (cold, deterministic init): the oracle's independent run
+    ol_q, oc_q, os_q = oracle_mod.kmeans(Q64, Cq, iters)
+    ol_k, oc_k, os_k = oracle_mod.kmeans(K64, Ck, iters)
+    assert np.array_equal(ex["q_labels"].cpu().numpy()[0, 0], ol_q)
+    assert np.array_equal(ex["k_labels"].cpu().numpy()[0, 0], ol_k)
+    assert np.array_equal(ex["q_centroids"].cpu().numpy()[0, 0], oc_q.astype(np.float32))
+    assert np.array_equal(ex["k_centroids"].cpu().numpy()[0, 0], oc_k.astype(np.float32))
+    # permutation
+    assert np.array_equal(ex["q_perm"].cpu().numpy()[0, 0], oracle_mod.permute(ol_q, Cq)[0])
+    assert np.array_equal(ex["k_perm"].cpu().numpy()[0, 0], oracle_mod.permute(ol_k, Ck)[0])
+    # selection on the GPU's f32 centroids (R22)
+    om, opairs, S, W, Z = oracle_mod.select_topp(ex["q_centroids"].cpu().numpy()[0, 0].astype(np.float64),
+                                                 ex["k_centroids"].cpu().numpy()[0, 0].astype(np.float64), os_q, os_k,
+                                                 d, f32scale(d), p, return_tables=True)
+    gm = ex["mask"].cpu().numpy()[0, 0]
+    nrows, nontie = mask_mismatch_rows_are_ties(W, Z, os_k, p, gm, om)
+    assert nontie == 0
+    if nrows == 0:
+        assert int(pairs[0, 0]) == opairs
+    ref = oracle_mod.attention_rows(Q64, K64, V64, f32scale(d), lq=ol_q, lk=ol_k, mask=gm)
+    check_attention(O[0, 0], ref, case)
+
+
+# ------------------------------------------------------------------ P7 and special cases
+@pytest.mark.parametrize("shape", [(1, 1, 1024, 1024, 64), (1, 2, 3000, 3000, 128)])
+def test_p1_equals_dense(svg2, oracle_mod, shape):
+    B, H, Nq, Nk, d = shape
+    q, k, v = random_qkv(B, H, Nq, Nk, d, seed=11)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O, pairs, _ = svg2.sparse_attention(Q, K, V, 8, 16, 2, 1.0)
+    assert torch.all(pairs == Nq * Nk)
+    Q64, K64, V64 = to_f64(Q), to_f64(K), to_f64(V)
+    for b in range(B):
+        for h in range(H):
+            check_attention(O[b, h], oracle_mod.dense_rows(Q64[b, h], K64[b, h], V64[b, h], f32scale(d)), "p=1")
+    # and against a plain PyTorch fp32 reference of the same op
+    ref = torch.softmax((Q.float() @ K.float().transpose(-1, -2)) * f32scale(d), -1) @ V.float()
+    assert (O.float() - ref).abs().max().item() <= MAX_ABS
+
+
+def test_single_cluster_is_dense(svg2, oracle_mod):
+    q, k, v = random_qkv(1, 1, 777, 777, 128, seed=12)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O, pairs, _ = svg2.sparse_attention(Q, K, V, 1, 1, 1, 0.5)
+    assert int(pairs[0, 0]) == 777 * 777
+    check_attention(O[0, 0], oracle_mod.dense_rows(to_f64(Q)[0, 0], to_f64(K)[0, 0], to_f64(V)[0, 0], f32scale(128)))
+
+
+def test_deterministic(svg2):
+    wl = svg2_synth.WORKLOADS["tiny"]
+    Q, K, V, Cq, Ck, p, iters = _pipeline_inputs(svg2, (2, 2, 5000, 5000, 128, 50, 100), seed=3)
+    O1, p1, e1 = svg2.sparse_attention(Q, K, V, Cq, Ck, iters, p)
+    O2, p2, e2 = svg2.sparse_attention(Q, K, V, Cq, Ck, iters, p)
+    assert torch.equal(O1, O2) and torch.equal(p1, p2) and torch.equal(e1["k_centroids"], e2["k_centroids"])
+
+
+def test_warm_start_cache(svg2):
+    q, k, v = random_qkv(1, 2, 3000, 3000, 128, seed=4)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    attn = svg2.SVG2Attention(Cq=20, Ck=50, top_p=0.9, iters_cold=30, iters_warm=1)
+    O1 = attn(Q, K, V)
+    cq = attn.q_centroids.clone()
+    O2 = attn(Q, K, V)  # converged cache: a warm step is (near) a fixed point
+    assert (attn.q_centroids - cq).abs().max().item() < 1e-3
+    assert (O1.float() - O2.float()).abs().max().item() < 5e-2
+
+
+def test_abi_errors(svg2):
+    q, k, v = random_qkv(1, 1, 256, 256, 64, seed=5)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    with pytest.raises(svg2.SVG2Error) as e:
+        svg2.sparse_attention(Q, K, V, 300, 8, 1, 0.9)  # C > N
+    assert e.value.status == 3
+    with pytest.raises(svg2.SVG2Error) as e:
+        svg2.sparse_attention(Q, K, V, 8, 8, 1, 1.5)  # top_p > 1
+    assert e.value.status == 3
+    with pytest.raises(svg2.SVG2Error) as e:
+        svg2.sparse_attention(Q, K, V, 8, 8, 0, 0.9)  # iters < 1
+    assert e.value.status == 3
+    bad = torch.empty(1, 1, 256, 48, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(svg2.SVG2Error) as e:
+        svg2.sparse_attention(bad, bad, bad, 8, 8, 1, 0.9)
+    assert e.value.status == 2
+    # the library still works after the rejected calls
+    O, _, _ = svg2.sparse_attention(Q, K, V, 8, 8, 1, 0.9)
+    torch.cuda.synchronize()
+    assert torch.isfinite(O.float()).all()
+
+
+# ------------------------------------------------------------------ full size, bench launch configuration
+@pytest.mark.parametrize("name", ["hunyuan720p"])
+def test_fullsize_sampled_rows(svg2, oracle_mod, name):
+    """BASELINE configs[1] at full size through the fused call (cold 5 iterations, then a warm 2-iteration call as
+    bench.py times it); the oracle checks sampled query rows of two heads, fed with the GPU's intermediates."""
+    wl = svg2_synth.WORKLOADS[name]
+    q, k, v = svg2_synth.generate(wl)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    del q, k, v
+    d = wl.d
+    _, _, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, wl.top_p)
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, wl.top_p, ex["q_centroids"], ex["k_centroids"],
+                                         warm=True, debug=True)
+    torch.cuda.synchronize()
+    dens = pairs.double() / (wl.N * wl.N)
+    assert 0.02 < float(dens.mean()) < 0.9
+    for h in (0, wl.H - 1):
+        rows = svg2_synth.sample_rows(wl.N, 256, seed=h)
+        Q64, K64, V64 = (to_f64(t[0, h]) for t in (Q, K, V))
+        lq, lk, m = (ex[n].cpu().numpy()[0, h] for n in ("q_labels", "k_labels", "mask"))
+        ref = oracle_mod.attention_rows(Q64, K64, V64, f32scale(d), rows=rows, lq=lq, lk=lk, mask=m)
+        check_attention(O[0, h][torch.from_numpy(rows).cuda()], ref, f"{name} head {h}")
+        # permutation and offsets of the final labels, bit-exact
+        p_ref, o_ref = oracle_mod.permute(lk, wl.Ck)
+        assert np.array_equal(ex["k_perm"].cpu().numpy()[0, h], p_ref)
+        assert np.array_equal(ex["k_offsets"].cpu().numpy()[0, h], o_ref)
+        # the returned centroids are the exact means of the returned clusters (f32-rounded)
+        ol, oc, osz = oracle_mod.kmeans(Q64, wl.Cq, 1, init=ex["q_centroids"].cpu().numpy()[0, h].astype(np.float64))
+        assert np.array_equal(np.bincount(lq, minlength=wl.Cq), ex["q_offsets"].cpu().numpy()[0, h][1:] -
+                              ex["q_offsets"].cpu().numpy()[0, h][:-1])
