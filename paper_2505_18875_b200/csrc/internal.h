@@ -39,16 +39,25 @@ inline SortWs carve_sort(Carver& c, int BH, int N, int C) {
   return w;
 }
 
+constexpr int kCentChunk = 128;  // centroids per tcgen05 N-chunk in the assign kernel
+inline int cent_pad(int C) { return (C + kCentChunk - 1) / kCentChunk * kCentChunk; }
+
 struct KmeansWs {
   SortWs sort;
-  int32_t* perm;     // [BH, N]   (used when the caller does not want perm)
-  int32_t* offsets;  // [BH, C+1]
+  int32_t* perm;      // [BH, N]   (used when the caller does not want perm)
+  int32_t* offsets;   // [BH, C+1]
+  uint16_t* c_hi;     // [BH, Cpad, d] bf16 hi part of the centroids (assign operand)
+  uint16_t* c_lo;     // [BH, Cpad, d] bf16 lo part: c - hi
+  float* c_norm;      // [BH, Cpad]  ||c||^2 (f32), +inf for padding centroids
 };
-inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C) {
+inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   KmeansWs w;
   w.sort = carve_sort(c, BH, N, C);
   w.perm = c.take<int32_t>(size_t(BH) * N);
   w.offsets = c.take<int32_t>(size_t(BH) * (C + 1));
+  w.c_hi = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
+  w.c_lo = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
+  w.c_norm = c.take<float>(size_t(BH) * cent_pad(C));
   return w;
 }
 

@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include "internal.h"
 #include "ptx.cuh"
+#include "tmap.h"
 
 namespace svg2 {
 namespace {
@@ -531,36 +532,12 @@ __global__ void __launch_bounds__(1024) k_flatten(int BH, int cap, AttnWs ws) {
   if (threadIdx.x == 0) *ws.n_items = base;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }
-  return fn;
-}
-
-bool make_map(CUtensorMap* m, const void* ptr, uint64_t rows, int d, uint32_t box_rows) {
-  auto enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t gdim[2] = {cuuint64_t(d), rows};
-  cuuint64_t gstr[1] = {cuuint64_t(d) * 2};
-  cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstr, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int D>
 cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int Ck, float scale,
                      const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s) {
   CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, Qp, uint64_t(BH) * Nq, D, 128) || !make_map(&mk, Kp, uint64_t(BH) * Nk, D, 1) ||
-      !make_map(&mv, Vp, uint64_t(BH) * Nk, D, 1))
+  if (!make_tmap_bf16(&mq, Qp, uint64_t(BH) * Nq, D, 128) || !make_tmap_bf16(&mk, Kp, uint64_t(BH) * Nk, D, 1) ||
+      !make_tmap_bf16(&mv, Vp, uint64_t(BH) * Nk, D, 1))
     return cudaErrorInvalidValue;
   Params p;
   p.items = ws.items;

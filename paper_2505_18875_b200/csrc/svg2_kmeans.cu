@@ -1,75 +1,187 @@
 // svg2_kmeans.cu — A1/A2/A5: Lloyd k-means per (b,h) on one role, warm-started from the caller's
 // centroid cache or from the deterministic strided cold init c_j = x[floor(j*N/C)] (DESIGN R2).
 //
-// One iteration = assign (argmin_j ||c_j||^2 - 2 x.c_j, f32; ties -> lowest j) -> stable sort of the labels
-// (svg2_permute.cu) -> centroid update c_j = (sum of its rows, fp64) / |cluster|, stored f32; empty clusters keep
-// their centroid (R6).  Sums of bf16 values in fp64 are exact at these magnitudes, so the update is order-free
-// and bit-identical to a sequential fp64 sum.
+// One iteration:
+//   k_centroid_split : c (f32) -> hi = bf16(c), lo = bf16(c - hi), ||c||^2 (f32); padded to 128-centroid chunks
+//   k_assign_tc      : the distance GEMM on tcgen05 — X tile (bf16, exact) x [hi | lo]^T accumulated in fp32 in TMEM
+//                      (K = 2d, so x.c carries ~16 mantissa bits of c), argmin_j ||c_j||^2 - 2 x.c_j read back with
+//                      tcgen05.ld (ties -> lowest j).  256 rows per CTA share every centroid chunk; chunks are
+//                      double-buffered in smem (TMA) and in TMEM (MMA of chunk c+1 overlaps the argmin of chunk c).
+//   stable sort of the labels (svg2_permute.cu)
+//   k_update         : c_j = (sum of its rows, fp64) / |cluster|, stored f32; empty clusters keep their centroid (R6).
+//                      Sums of bf16 values in fp64 are exact at these magnitudes, so the update is order-free and
+//                      bit-identical to the oracle's sequential sum.
 #include <cuda_bf16.h>
 #include "internal.h"
+#include "ptx.cuh"
+#include "tmap.h"
 
 namespace svg2 {
 namespace {
 
-constexpr int kAssignRows = 128;  // rows per block (one row per thread, the row lives in registers)
-constexpr int kCentChunk = 64;    // centroids staged in shared memory per pass
+constexpr int kAsgThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 argmin epilogue (2 row tiles x 4 warps)
+constexpr int kAsgRows = 256;     // rows per CTA (two 128-row M tiles sharing each centroid chunk)
 
 template <int D>
-__global__ void __launch_bounds__(kAssignRows) k_assign(const __nv_bfloat16* __restrict__ X, int N, int C,
-                                                        const float* __restrict__ cent, int32_t* __restrict__ labels) {
-  __shared__ __align__(16) float sc[kCentChunk * D];
-  __shared__ float sn[kCentChunk];
-  const int bh = blockIdx.y;
-  const int n = blockIdx.x * kAssignRows + threadIdx.x;
-  float x[D];
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(X + (size_t(bh) * N + min(n, N - 1)) * D);
-#pragma unroll
-    for (int v = 0; v < D / 8; ++v) {
-      uint4 u = __ldg(src + v);
-      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 f = __bfloat1622float2(p[e]);
-        x[8 * v + 2 * e] = f.x;
-        x[8 * v + 2 * e + 1] = f.y;
+struct AsgCfg {
+  static constexpr int kBlocks = D / 64;
+  static constexpr uint32_t kBlockBytes = 128 * 128;            // 128 rows x 64 bf16
+  static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;  // 128 rows x D bf16
+  static constexpr uint32_t kNormBytes = kMaxClusters * 4;
+  static constexpr uint32_t kSmem = 2 * kTileBytes + 4 * kTileBytes + kNormBytes + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(D) k_centroid_split(const float* __restrict__ cent, int C, int Cpad,
+                                                      __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+                                                      float* __restrict__ norm) {
+  __shared__ float red[D / 32];
+  const int j = blockIdx.x, bh = blockIdx.y, k = threadIdx.x;
+  const float c = j < C ? cent[(size_t(bh) * C + j) * D + k] : 0.f;
+  const __nv_bfloat16 h = __float2bfloat16_rn(c);
+  const __nv_bfloat16 l = __float2bfloat16_rn(c - __bfloat162float(h));
+  hi[(size_t(bh) * Cpad + j) * D + k] = h;
+  lo[(size_t(bh) * Cpad + j) * D + k] = l;
+  float s = c * c;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((k & 31) == 0) red[k >> 5] = s;
+  __syncthreads();
+  if (k == 0) {
+    float t = 0.f;
+    for (int w = 0; w < D / 32; ++w) t += red[w];
+    norm[size_t(bh) * Cpad + j] = j < C ? t : INFINITY;
+  }
+}
+
+struct AsgBars {
+  uint64_t x_full, c_full[2], c_empty[2], acc_full[2], acc_empty[2];
+};
+
+template <int D>
+__global__ void __launch_bounds__(kAsgThreads, 1)
+    k_assign_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
+                const __grid_constant__ CUtensorMap mapLo, const float* __restrict__ c_norm, int N, int Cpad,
+                int32_t* __restrict__ labels) {
+  using C = AsgCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sX = smem;                       // [2 tiles]
+  uint8_t* sH = smem + 2 * C::kTileBytes;   // [2 stages]
+  uint8_t* sL = sH + 2 * C::kTileBytes;     // [2 stages]
+  float* sNorm = reinterpret_cast<float*>(sL + 2 * C::kTileBytes);  // [Cpad]
+  __shared__ AsgBars bars;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.y, row0 = blockIdx.x * kAsgRows;
+  const int ntile = (row0 + 128 < N) ? 2 : 1;
+  const int nchunks = Cpad / kCentChunk;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&mapX);
+    tma_prefetch_desc(&mapHi);
+    tma_prefetch_desc(&mapLo);
+    mbar_init(&bars.x_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.c_full[s], 1);
+      mbar_init(&bars.c_empty[s], 1);
+      mbar_init(&bars.acc_full[s], 1);
+      mbar_init(&bars.acc_empty[s], 4 * ntile);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&tmem_slot);
+  for (int j = threadIdx.x; j < Cpad; j += kAsgThreads) sNorm[j] = __ldg(c_norm + size_t(bh) * Cpad + j);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int xrow = bh * N + row0;
+      mbar_arrive_expect_tx(&bars.x_full, ntile * C::kTileBytes);
+      for (int t = 0; t < ntile; ++t)
+        for (int b = 0; b < C::kBlocks; ++b)
+          tma_load_2d(sX + t * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full, 64 * b, xrow + 128 * t);
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c & 1;
+        const uint32_t ph = (c >> 1) & 1;
+        mbar_wait(&bars.c_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&bars.c_full[s], 2 * C::kTileBytes);
+        const int crow = bh * Cpad + c * kCentChunk;
+        for (int b = 0; b < C::kBlocks; ++b) {
+          tma_load_2d(sH + s * C::kTileBytes + b * C::kBlockBytes, &mapHi, &bars.c_full[s], 64 * b, crow);
+          tma_load_2d(sL + s * C::kTileBytes + b * C::kBlockBytes, &mapLo, &bars.c_full[s], 64 * b, crow);
+        }
       }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(128, kCentChunk, false);
+      mbar_wait(&bars.x_full, 0);
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c & 1;
+        const uint32_t ph = (c >> 1) & 1;
+        mbar_wait(&bars.c_full[s], ph);
+        mbar_wait(&bars.acc_empty[s], ph ^ 1);
+        tc_fence_after();
+        const uint32_t h = smem_u32(sH + s * C::kTileBytes), l = smem_u32(sL + s * C::kTileBytes);
+        for (int t = 0; t < ntile; ++t) {
+          const uint32_t x = smem_u32(sX + t * C::kTileBytes);
+          const uint32_t dcol = tmem + (s * 2 + t) * 128;
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+            mma_ss(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(h + off), idesc, k > 0);
+          }
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+            mma_ss(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(l + off), idesc, 1u);
+          }
+        }
+        mma_commit(&bars.c_empty[s]);
+        mma_commit(&bars.acc_full[s]);
+      }
+    }
+  } else {
+    const int t = (warp - 2) >> 2;
+    if (t < ntile) {
+      const int quarter = warp & 3;
+      const int row = row0 + t * 128 + quarter * 32 + lane;
+      const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+      float best = INFINITY;
+      int bj = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c & 1;
+        const uint32_t ph = (c >> 1) & 1;
+        mbar_wait(&bars.acc_full[s], ph);
+        tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < kCentChunk / 32; ++q) {
+          uint32_t r[32];
+          tmem_ld32(tmem + lane_addr + (s * 2 + t) * 128 + 32 * q, r);
+          tmem_wait_ld();
+          const int j0 = c * kCentChunk + 32 * q;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float dist = fmaf(-2.f, __uint_as_float(r[e]), sNorm[j0 + e]);
+            if (dist < best) {  // strict: ties keep the lower index
+              best = dist;
+              bj = j0 + e;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.acc_empty[s]);
+      }
+      if (row < N) labels[size_t(bh) * N + row] = bj;
     }
   }
-  const float* cb = cent + size_t(bh) * C * D;
-  float best = INFINITY;
-  int bj = 0;
-  for (int j0 = 0; j0 < C; j0 += kCentChunk) {
-    const int cnt = min(kCentChunk, C - j0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt * D / 4; t += kAssignRows)
-      reinterpret_cast<float4*>(sc)[t] = __ldg(reinterpret_cast<const float4*>(cb + size_t(j0) * D) + t);
-    __syncthreads();
-    if (threadIdx.x < cnt) {
-      float s = 0.f;
-      for (int k = 0; k < D; ++k) s = fmaf(sc[threadIdx.x * D + k], sc[threadIdx.x * D + k], s);
-      sn[threadIdx.x] = s;
-    }
-    __syncthreads();
-    for (int jj = 0; jj < cnt; ++jj) {
-      const float4* c4 = reinterpret_cast<const float4*>(sc + jj * D);
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-      for (int k4 = 0; k4 < D / 4; ++k4) {
-        const float4 c = c4[k4];
-        a0 = fmaf(x[4 * k4 + 0], c.x, a0);
-        a1 = fmaf(x[4 * k4 + 1], c.y, a1);
-        a2 = fmaf(x[4 * k4 + 2], c.z, a2);
-        a3 = fmaf(x[4 * k4 + 3], c.w, a3);
-      }
-      const float dist = fmaf(-2.f, (a0 + a1) + (a2 + a3), sn[jj]);
-      if (dist < best) {  // strict: ties keep the lower index
-        best = dist;
-        bj = j0 + jj;
-      }
-    }
-  }
-  if (n < N) labels[size_t(bh) * N + n] = bj;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 template <int D>
@@ -115,9 +227,19 @@ template <int D>
 cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, float* cent, int32_t* labels,
                        int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws, cudaStream_t s) {
   const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(Xv);
+  const int Cpad = cent_pad(C);
+  CUtensorMap mx, mh, ml;
+  if (!make_tmap_bf16(&mx, Xv, uint64_t(BH) * N, D, 128) || !make_tmap_bf16(&mh, ws.c_hi, uint64_t(BH) * Cpad, D, 128) ||
+      !make_tmap_bf16(&ml, ws.c_lo, uint64_t(BH) * Cpad, D, 128))
+    return cudaErrorInvalidValue;
+  cudaFuncSetAttribute(k_assign_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<D>::kSmem);
   if (!warm) k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
+  __nv_bfloat16* hi = reinterpret_cast<__nv_bfloat16*>(ws.c_hi);
+  __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
   for (int it = 0; it < iters; ++it) {
-    k_assign<D><<<dim3((N + kAssignRows - 1) / kAssignRows, BH), kAssignRows, 0, s>>>(X, N, C, cent, labels);
+    k_centroid_split<D><<<dim3(Cpad, BH), D, 0, s>>>(cent, C, Cpad, hi, lo, ws.c_norm);
+    k_assign_tc<D><<<dim3((N + kAsgRows - 1) / kAsgRows, BH), kAsgThreads, AsgCfg<D>::kSmem, s>>>(
+        mx, mh, ml, ws.c_norm, N, Cpad, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
     k_update<D><<<dim3(C, BH), D / 2, 0, s>>>(X, N, C, perm, offsets, cent);
@@ -127,7 +249,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
 
 }  // namespace
 
-int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * (2 + kSortLaunches); }
+int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * (3 + kSortLaunches); }
 
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
