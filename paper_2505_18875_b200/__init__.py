@@ -149,7 +149,7 @@ def kmeans(X: torch.Tensor, C: int, iters: int, centroids: torch.Tensor | None =
     perm = torch.empty(B, H, N, dtype=torch.int32, device=X.device) if return_perm else None
     offsets = torch.empty(B, H, C + 1, dtype=torch.int32, device=X.device) if return_perm else None
     nbytes = workspace_size(ENTRY_KMEANS, B, H, N, N, d, C, iters=iters)
-    ws = _workspace(nbytes, X.device)
+    ws = _workspace(max(nbytes, 256), X.device)
     _check("svg2_kmeans", lib.svg2_kmeans(_p(X), B, H, N, d, C, iters, SVG2_WARM_START if warm else 0, _p(centroids),
                                           _p(labels), _p(sizes), _p(perm), _p(offsets), _p(ws), ws.numel(),
                                           _stream()))
@@ -177,7 +177,7 @@ def permute(labels: torch.Tensor, C: int, X0: torch.Tensor | None = None, X1: to
     X0p = torch.empty_like(X0) if X0 is not None else None
     X1p = torch.empty_like(X1) if X1 is not None else None
     nbytes = workspace_size(ENTRY_PERMUTE, B, H, N, N, d, C)
-    ws = _workspace(nbytes, labels.device)
+    ws = _workspace(max(nbytes, 256), labels.device)
     _check("svg2_permute", lib.svg2_permute(_p(labels), B, H, N, d, C, _p(X0), _p(X0p), _p(X1), _p(X1p), _p(perm),
                                             _p(offsets), _p(ws), ws.numel(), _stream()))
     return perm, offsets, X0p, X1p
@@ -213,7 +213,7 @@ def varblock_attention(Qp, Kp, Vp, q_offsets, k_offsets, mask, scale: float = 0.
     O = torch.empty_like(Qp)
     lse = torch.empty(B, H, Nq, dtype=torch.float32, device=Qp.device) if return_lse else None
     nbytes = workspace_size(ENTRY_VARBLOCK_ATTENTION, B, H, Nq, Nk, d, Cq, Ck)
-    ws = _workspace(nbytes, Qp.device)
+    ws = _workspace(max(nbytes, 256), Qp.device)
     _check("svg2_varblock_attention",
            lib.svg2_varblock_attention(_p(Qp), _p(Kp), _p(Vp), Dims(B, H, Nq, Nk, d), _p(q_offsets), _p(k_offsets),
                                        _p(mask), Cq, Ck, scale, _p(q_perm), _p(O), _p(lse), _p(ws), ws.numel(),
@@ -260,10 +260,9 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
     pairs = torch.empty(B, H, dtype=torch.int64, device=dev)
     cfg = Config(Cq, Ck, iters, top_p, scale, SVG2_WARM_START if warm else 0)
     dims = Dims(B, H, Nq, Nk, d)
+    # 0 = invalid arguments: still call the ABI so the caller gets its precise status code
     nbytes = int(lib.svg2_workspace_size(ENTRY_SPARSE_ATTENTION, dims, ctypes.byref(cfg)))
-    if nbytes == 0:
-        raise SVG2Error("svg2_workspace_size", 3)
-    ws = _workspace(nbytes, dev)
+    ws = _workspace(max(nbytes, 256), dev)
     extras = {"q_centroids": q_centroids, "k_centroids": k_centroids}
     dbg = None
     if debug or events is not None:
@@ -281,7 +280,11 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
                 setattr(dbg, name, extras[name].data_ptr())
         if events is not None:
             for i, ev in enumerate(events[:8]):
-                dbg.events[i] = ev.cuda_event if ev is not None else None
+                if ev is None:
+                    continue
+                if not ev.cuda_event:  # torch creates events lazily: record once so a handle exists
+                    ev.record()
+                dbg.events[i] = ev.cuda_event
     _check("svg2_sparse_attention",
            lib.svg2_sparse_attention(_p(Q), _p(K), _p(V), dims, ctypes.byref(cfg), _p(q_centroids), _p(k_centroids),
                                      _p(O), _p(pairs), ctypes.byref(dbg) if dbg is not None else None, _p(ws),

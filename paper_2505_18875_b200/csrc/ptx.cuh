@@ -13,6 +13,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 namespace svg2 {
 
@@ -65,11 +66,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // Watchdog: a pipeline that has not advanced for kMbarTimeoutNs traps (the launch fails with an error)
 // instead of hanging the device.
 constexpr uint64_t kMbarTimeoutNs = 10ull * 1000 * 1000 * 1000;
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(bar, parity)) {
-    if (globaltimer_ns() - t0 > kMbarTimeoutNs) __trap();
+    if (globaltimer_ns() - t0 > kMbarTimeoutNs) {
+      if ((threadIdx.x & 31) == 0)
+        printf("svg2 watchdog: block %d thread %d wait-site %d parity %u stalled > 10 s\n", int(blockIdx.x),
+               int(threadIdx.x), tag, parity);
+      __trap();
+    }
   }
 }
 

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nkeys = item_keys(p, it);
       const int2* runs = p.runs + size_t(it.z) * p.Ck;
       const int rc = __ldg(p.run_count + it.z);
-      mbar_wait(&bars.q_empty, qph ^ 1);
+      mbar_wait(&bars.q_empty, qph ^ 1, 1);
       if (lane == 0) {
         mbar_arrive_expect_tx(&bars.q_full, (nb > 0 ? 2u : 1u) * C::kTileBytes);
         for (int b = 0; b < C::kBlocks; ++b) {
@@ -196,13 +196,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < T; ++t) {
         int rows[4];
         tile_rows(runs, rc, r, off, t * kKTile, nkeys, lane, rows);
-        mbar_wait(&bars.k_empty[ks], kph ^ 1);
+        mbar_wait(&bars.k_empty[ks], kph ^ 1, 2);
         if (lane == 0) mbar_arrive_expect_tx(&bars.k_full[ks], C::kTileBytes);
         __syncwarp();
         uint8_t* dk = sK + ks * C::kTileBytes + lane * 512;
         for (int b = 0; b < C::kBlocks; ++b)
           tma_gather4(dk + b * C::kBlockBytes, &mapK, &bars.k_full[ks], 64 * b, rows[0], rows[1], rows[2], rows[3]);
-        mbar_wait(&bars.v_empty[ks], kph ^ 1);
+        mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
         if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], C::kTileBytes);
         __syncwarp();
         uint8_t* dv = sV + ks * C::kTileBytes + lane * 512;
@@ -250,10 +250,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ts(dcol, pcol + 8 * k, desc_mnmajor_sw128(vb + k * 16 * 128, C::kBlockBytes), idesc_pv,
                  (t > 0 || k > 0) ? 1u : 0u);
       };
-      mbar_wait(&bars.q_full, qph);
+      mbar_wait(&bars.q_full, qph, 4);
       qph ^= 1;
       // prologue: S(0)
-      mbar_wait(&bars.k_full[ks], kph);
+      mbar_wait(&bars.k_full[ks], kph, 5);
       tc_fence_after();
       if (lane == 0) {
         issue_s(0, 0, ks);
@@ -272,13 +272,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int t = 0; t < T; ++t) {
         const bool more = t + 1 < T;
-        mbar_wait(&bars.v_full[vs], vph);
-        if (more) mbar_wait(&bars.k_full[ks], kph);
+        mbar_wait(&bars.v_full[vs], vph, 6);
+        if (more) mbar_wait(&bars.k_full[ks], kph, 7);
         // ---- tile a
-        mbar_wait(&bars.p_full[0], pph[0]);
+        mbar_wait(&bars.p_full[0], pph[0], 8);
         pph[0] ^= 1;
         if (t == 0) {
-          mbar_wait(&bars.o_empty[0], oeph[0] ^ 1);
+          mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
           oeph[0] ^= 1;
         }
         tc_fence_after();
@@ -294,10 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         // ---- tile b
         if (has_b) {
-          mbar_wait(&bars.p_full[1], pph[1]);
+          mbar_wait(&bars.p_full[1], pph[1], 10);
           pph[1] ^= 1;
           if (t == 0) {
-            mbar_wait(&bars.o_empty[1], oeph[1] ^ 1);
+            mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
             oeph[1] ^= 1;
           }
           tc_fence_after();
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m_used = -INFINITY, l = 0.f;
       for (int t = 0; t < T; ++t) {
         const int nvalid = min(kKTile, nkeys - t * kKTile);
-        mbar_wait(&bars.s_full[g], sph);
+        mbar_wait(&bars.s_full[g], sph, 12 + g);
         sph ^= 1;
         tc_fence_after();
         uint32_t s0[32], s1[32], s2[32], s3[32];
@@ -374,8 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         scale_mask(s3, 96);
         if (t == 0) {
           m_used = mt;
-        } else if (mt > m_used + kRescaleThreshold) {
-          const float alpha = ex2_approx(m_used - mt);
+        } else if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+          // warp-uniform branch (tcgen05.ld/st are .sync.aligned); rows whose max did not grow get alpha = 1
+          const float m_new = fmaxf(m_used, mt);
+          const float alpha = ex2_approx(m_used - m_new);
           l *= alpha;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
             tmem_st32(tO + 32 * c, o);
           }
-          m_used = mt;
+          m_used = m_new;
         }
         float lsum = 0.f;
         auto exp_store = [&](const uint32_t(&a)[32], int c) {
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&bars.p_full[g]);
       }
       // ---- epilogue: O / l  -> bf16 -> original token order (fused pi_q^T)
-      mbar_wait(&bars.o_full[g], oph);
+      mbar_wait(&bars.o_full[g], oph, 14 + g);
       oph ^= 1;
       tc_fence_after();
       const float inv_l = 1.f / l;

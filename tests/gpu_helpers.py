@@ -20,11 +20,13 @@ def random_qkv(B, H, Nq, Nk, d, seed, amp=3.0, groups=8):
     """Clustered random inputs (not the synth recipe): useful for ragged / odd shapes."""
     rng = np.random.default_rng(seed)
     out = []
-    for N in (Nq, Nk, Nk):
+    for N in (Nq, Nk):  # clustered Q and K
         mu = rng.standard_normal((groups, d)).astype(np.float32)
         g = rng.integers(0, groups, (B, H, N))
         x = mu[g] * amp + rng.standard_normal((B, H, N, d)).astype(np.float32)
         out.append(svg2_synth.f32_to_bf16_bits(x))
+    # V ~ N(0, I) as in the svg2-synth recipe: O(1) outputs, the scale the 2e-2 / 2e-3 tolerances are written for
+    out.append(svg2_synth.f32_to_bf16_bits(rng.standard_normal((B, H, Nk, d)).astype(np.float32)))
     return out
 
 
