@@ -61,25 +61,35 @@ inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   return w;
 }
 
+// Key stream of one query cluster = its selected key clusters' rows in K'/V', adjacent clusters merged into runs,
+// every run padded to whole 8-row groups.  A group = (first row in the flattened [BH*Nk] key tensor, #valid rows
+// 0..8).  The stream is padded to an even number of groups so every tile has N = 16*k keys.  Tile t = groups
+// [16t, 16t+16); its 16 valid counts are also packed 4 bits each into one 64-bit tile word for the softmax mask.
+inline size_t group_cap(int Nk, int Ck) { return size_t(Nk) / 8 + size_t(Ck) + 2; }
+inline size_t tile_cap(int Nk, int Ck) { return group_cap(Nk, Ck) / 16 + 1; }
+
 struct AttnWs {
-  int2* runs;          // [BH, Cq, Ck]  (absolute first row in the flattened [BH*Nk] key tensor, length)
-  int32_t* run_count;  // [BH, Cq]
-  int32_t* nkeys;      // [BH, Cq]
+  int2* groups;        // [BH, Cq, group_cap]
+  uint64_t* tilew;     // [BH, Cq, tile_cap]
+  int32_t* ngroups;    // [BH, Cq]
   int4* items_bh;      // [BH, cap]
   int32_t* items_cnt;  // [BH]
   int4* items;         // [BH * cap] flattened
-  int32_t* n_items;    // [1]
+  int32_t* n_items;    // [2]: item count, dynamic-scheduler counter
+  size_t gcap, tcap;
 };
-inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Cq, int Ck) {
+inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Nk, int Cq, int Ck) {
   AttnWs w;
   const size_t cap = items_cap_per_bh(Nq, Cq);
-  w.runs = c.take<int2>(size_t(BH) * Cq * Ck);
-  w.run_count = c.take<int32_t>(size_t(BH) * Cq);
-  w.nkeys = c.take<int32_t>(size_t(BH) * Cq);
+  w.gcap = group_cap(Nk, Ck);
+  w.tcap = tile_cap(Nk, Ck);
+  w.groups = c.take<int2>(size_t(BH) * Cq * w.gcap);
+  w.tilew = c.take<uint64_t>(size_t(BH) * Cq * w.tcap);
+  w.ngroups = c.take<int32_t>(size_t(BH) * Cq);
   w.items_bh = c.take<int4>(size_t(BH) * cap);
   w.items_cnt = c.take<int32_t>(BH);
   w.items = c.take<int4>(size_t(BH) * cap);
-  w.n_items = c.take<int32_t>(1);
+  w.n_items = c.take<int32_t>(2);
   return w;
 }
 

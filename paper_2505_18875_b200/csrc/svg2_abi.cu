@@ -72,7 +72,7 @@ FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) 
   Carver km(c.base ? c.base + start : nullptr);
   w.km = probe_q.off >= probe_k.off ? carve_kmeans(km, int(BH), dm.Nq, cfg.Cq) : carve_kmeans(km, int(BH), dm.Nk, cfg.Ck);
   c.off = start + km.off;
-  w.attn = carve_attn(c, int(BH), dm.Nq, cfg.Cq, cfg.Ck);
+  w.attn = carve_attn(c, int(BH), dm.Nq, dm.Nk, cfg.Cq, cfg.Ck);
   return w;
 }
 
@@ -131,7 +131,7 @@ size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dm, const svg2_config
       if (check_bhnd(dm.B, dm.H, dm.Nq, dm.d) != SVG2_OK || check_bhnd(dm.B, dm.H, dm.Nk, dm.d) != SVG2_OK ||
           check_clusters(cfg->Cq, dm.Nq) != SVG2_OK || check_clusters(cfg->Ck, dm.Nk) != SVG2_OK)
         return 0;
-      carve_attn(c, int(BH), dm.Nq, cfg->Cq, cfg->Ck);
+      carve_attn(c, int(BH), dm.Nq, dm.Nk, cfg->Cq, cfg->Ck);
       return c.off + 256;
     case SVG2_ENTRY_SPARSE_ATTENTION:
       if (validate_fused(dm, cfg) != SVG2_OK) return 0;
@@ -217,7 +217,7 @@ svg2_status_t svg2_varblock_attention(const void* Qp, const void* Kp, const void
   if ((st = pending_error()) != SVG2_OK) return st;
   Carver c(ws);
   const int BH = dm.B * dm.H;
-  AttnWs aw = carve_attn(c, BH, dm.Nq, Cq, Ck);
+  AttnWs aw = carve_attn(c, BH, dm.Nq, dm.Nk, Cq, Ck);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = launch_build_worklist(q_offsets, k_offsets, mask, BH, dm.Nq, dm.Nk, Cq, Ck, aw, s);
   if (e == cudaSuccess)

@@ -1,15 +1,17 @@
 // svg2_attn.cu — A9 (+ fused A10): dynamic-block-size sparse attention over the permuted, cluster-contiguous
 // tokens, written for sm_100a.
 //
-// Work item = two 128-row Q tiles of one query cluster i (contiguous rows of Q' after the permutation) sharing
-// ONE packed key stream: the concatenation of the selected key clusters' row ranges of K'/V' (adjacent selected
-// clusters merged into runs).  The paper loads K/V "sparsely per token via address offsets into contiguous
-// shared memory"; here every 128-key tile of the packed stream is assembled by TMA gather4 (4
-// arbitrary rows per instruction) straight into 128B-swizzled shared memory, so there is no per-cluster padding:
-// only the last tile of a stream is partial (its N is rounded up to 16 and the tail columns are masked).
+// Work item = two 128-row Q tiles of one query cluster i (contiguous rows of Q' after the permutation) sharing ONE
+// packed key stream: the selected key clusters' row ranges of K'/V' (adjacent selected clusters merged into runs),
+// each run padded to whole 8-row groups.  The paper loads K/V "sparsely per token via address offsets into
+// contiguous shared memory"; here a 128-key tile of the stream (16 groups) is assembled from TMA box
+// loads straight into the 128B-swizzled layout the MMA descriptors expect: consecutive groups of one run merge into
+// power-of-two boxes of 8..128 rows, so a tile typically costs 1-3 box loads per 64-column half.  Padding rows of a
+// run's last group are masked in the softmax (a 4-bit valid count per group, packed per tile).
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent over the work list):
-//   warp 0      TMA producer: Q tiles (box loads), K/V tiles (gather4) into a 2-stage ring each
+// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter):
+//   warp 0      scheduler + TMA producer: fetches the next item, broadcasts it through a 2-slot smem ring, loads
+//               the Q tiles (box loads) and the K/V tiles (box loads) into 2-stage rings
 //   warp 1      MMA issuer (one thread): S = Q K^T (SS, K-major both) into TMEM; O += P V (TS: P read from TMEM,
 //               V MN-major) -- ping-pong order PV_a(t), S_a(t+1), PV_b(t), S_b(t+1)
 //   warp 2      TMEM allocator (512 columns: S_a | S_b | O_a | O_b)
@@ -23,24 +25,30 @@
 #include "internal.h"
 #include "ptx.cuh"
 #include "tmap.h"
+#include <cstdlib>
 
 namespace svg2 {
 namespace {
 
 constexpr int kThreads = 384;
 constexpr int kStages = 2;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 256 between rescales
-constexpr int kRunSentinelLen = 1 << 20;
+constexpr int kGroupsPerTile = kKTile / 8;  // 16
+constexpr int kBoxKinds = 5;                // box heights 8, 16, 32, 64, 128 rows
+constexpr float kRescaleThreshold = 8.0f;   // log2 units: P <= 256 between rescales
+constexpr uint64_t kFullTileWord = 0x8888888888888888ull;
 // setmaxnreg budget: the launch reserves 168 regs x 384 threads; warpgroup 0 (producer / MMA / TMEM) shrinks to
 // 72 and the two softmax warpgroups grow to 216.  The sum must not exceed the reservation or .inc never returns.
 constexpr int kRegsCtl = 72, kRegsSoftmax = 216, kRegsLaunch = 168;
 static_assert(128 * kRegsCtl + 256 * kRegsSoftmax <= kRegsLaunch * kThreads, "setmaxnreg budget exceeds launch");
+constexpr int kItemConsumers = 1 + 8;  // MMA warp + 8 softmax warps arrive on item_empty
+constexpr int kDefaultPolyStride = 0;
 
 template <int D>
 struct Cfg {
   static constexpr int kBlocks = D / 64;               // 64-column (128-byte) swizzle blocks per row
   static constexpr uint32_t kBlockBytes = 128 * 128;   // one 64-column block of a 128-row tile
   static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;
+  static constexpr uint32_t kGroupBytes = 8 * 2 * D;   // 8 rows x D bf16
   static constexpr uint32_t kSmemBytes = (2 + 2 * kStages) * kTileBytes + 1024;
   static constexpr uint32_t kColSa = 0, kColSb = 128, kColOa = 256, kColOb = 384;
 };
@@ -49,90 +57,61 @@ struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t item_full[2], item_empty[2];
+};
+
+struct KVMaps {
+  CUtensorMap k[kBoxKinds], v[kBoxKinds];  // box = 64 columns x (8 << kind) rows
 };
 
 struct Params {
   const int4* items;
-  const int32_t* n_items;
-  const int2* runs;
-  const int32_t* run_count;
-  const int32_t* nkeys;
+  int32_t* n_items;  // [0] = count, [1] = dynamic-scheduler counter (zeroed by k_flatten)
+  const int2* groups;
+  const uint64_t* tilew;
+  const int32_t* ngroups;
+  size_t gcap, tcap;
   const int32_t* q_perm;
   __nv_bfloat16* O;
   float* lse;
-  int Nq, Ck;
+  int Nq;
   float scale_log2;
 };
 
-__device__ __forceinline__ int item_keys(const Params& p, int4 it) { return __ldg(p.nkeys + it.z); }
-
-// The 4 key rows lane `lane` gathers for tile positions [4*lane, 4*lane+4) of the packed stream.
-// State (r, off): the tile starts at offset `off` inside run r of this item's run list.  Runs are read 32 at a
-// time (one per lane); an inclusive prefix over their lengths resolves each position with a 5-step shuffle
-// binary search.  Positions past the end of the stream get the stream's first row (masked later).
-__device__ __forceinline__ void tile_rows(const int2* __restrict__ runs, int rc, int& r, int& off, int tile_base,
-                                          int nkeys, int lane, int (&rows)[4]) {
-  int first_row = __ldg(&runs[0].x);
-  bool done[4] = {false, false, false, false};
-#pragma unroll
-  for (int c = 0; c < 4; ++c) rows[c] = first_row;
-  int base = 0;  // tile-relative position where the current window starts
-  int wr = r, woff = off;
-  while (true) {
-    int2 run = (wr + lane < rc) ? __ldg(runs + wr + lane) : make_int2(first_row, kRunSentinelLen);
-    int len = run.y - (lane == 0 ? woff : 0);
-    int start = run.x + (lane == 0 ? woff : 0);
-    int incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+// Loads one 16-group tile of the item's key stream into a K or V stage.  Lanes 0..ngt-1 hold one group each; a
+// lane whose group does not continue the previous lane's full group starts a run segment and issues power-of-two
+// boxes covering it.  The stage's mbarrier receives ngt x 8 rows x D x 2 bytes.
+template <int D>
+__device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* stage, uint64_t* bar, int ngt, int lane,
+                                             int2 gw) {
+  using C = Cfg<D>;
+  const int prev_row = __shfl_up_sync(0xffffffffu, gw.x, 1);
+  const int prev_nv = __shfl_up_sync(0xffffffffu, gw.y, 1);
+  const bool in = lane < ngt;
+  const bool cont = in && lane > 0 && gw.x == prev_row + 8 && prev_nv == 8;
+  const bool start = in && !cont;
+  const unsigned starts = __ballot_sync(0xffffffffu, start);
+  if (start) {
+    const unsigned above = starts & ~((2u << lane) - 1u);
+    const int end = above ? (__ffs(above) - 1) : ngt;
+    int pos = lane, len = end - lane, row = gw.x;
+    while (len > 0) {
+      const int kind = 31 - __clz(min(len, 16));  // largest power of two <= len, capped at 16 groups (128 rows)
+      const int pw = 1 << kind;
+      for (int b = 0; b < C::kBlocks; ++b)
+        tma_load_2d(stage + b * C::kBlockBytes + pos * 1024, &maps[kind], bar, 64 * b, row);
+      pos += pw;
+      len -= pw;
+      row += 8 * pw;
     }
-    const int covered = __shfl_sync(0xffffffffu, incl, 31);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int P = 4 * lane + c - base;
-      // first window lane j with incl_j > P
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-        if (v <= P) lo += step;
-      }
-      const int ij = __shfl_sync(0xffffffffu, incl, lo);
-      const int lj = __shfl_sync(0xffffffffu, len, lo);
-      const int sj = __shfl_sync(0xffffffffu, start, lo);
-      if (!done[c] && P >= 0 && P < covered) {
-        const int gpos = tile_base + 4 * lane + c;
-        rows[c] = gpos < nkeys ? sj + (P - (ij - lj)) : first_row;
-        done[c] = true;
-      }
-    }
-    if (base + covered >= kKTile) {
-      // next tile starts at window position kKTile - base
-      const int Pn = kKTile - base;
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-        if (v <= Pn) lo += step;
-      }
-      const int ij = __shfl_sync(0xffffffffu, incl, lo);
-      const int lj = __shfl_sync(0xffffffffu, len, lo);
-      r = wr + lo;
-      off = (lo == 0 ? woff : 0) + (Pn - (ij - lj));
-      return;
-    }
-    base += covered;
-    wr += 32;
-    woff = 0;
   }
 }
 
-template <int D>
+// kPolyStride > 0: one pair of elements in every kPolyStride takes exp2 on the FMA pipes (ex2_poly) instead of
+// MUFU, balancing the two units (FA4's partial software exp2).
+template <int D, int kPolyStride>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_varblock_attn(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-                    const __grid_constant__ CUtensorMap mapV, const Params p) {
+    k_varblock_attn(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ KVMaps kv, const Params p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -141,12 +120,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = sK + kStages * C::kTileBytes;        // [kStages][tile]
   __shared__ Bars bars;
   __shared__ uint32_t tmem_slot;
+  __shared__ int4 item_slot[2];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapQ);
-    tma_prefetch_desc(&mapK);
-    tma_prefetch_desc(&mapV);
     mbar_init(&bars.q_full, 1);
     mbar_init(&bars.q_empty, 1);
     for (int s = 0; s < kStages; ++s) {
@@ -160,6 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars.p_full[g], 4);
       mbar_init(&bars.o_full[g], 1);
       mbar_init(&bars.o_empty[g], 4);
+      mbar_init(&bars.item_full[g], 1);
+      mbar_init(&bars.item_empty[g], kItemConsumers);
     }
     fence_mbar_init();
   }
@@ -171,166 +151,179 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_items = __ldg(p.n_items);
 
   if (warp < 4) {
-  reg_dealloc<kRegsCtl>();
-  if (warp == 0) {
-    // ============================ TMA producer ============================
-    uint32_t qph = 0, ks = 0, kph = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int4 it = __ldg(p.items + item);
-      const int na = it.y & 0xFFFF, nb = it.y >> 16;
-      const int nkeys = item_keys(p, it);
-      const int2* runs = p.runs + size_t(it.z) * p.Ck;
-      const int rc = __ldg(p.run_count + it.z);
-      mbar_wait(&bars.q_empty, qph ^ 1, 1);
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&bars.q_full, (nb > 0 ? 2u : 1u) * C::kTileBytes);
-        for (int b = 0; b < C::kBlocks; ++b) {
-          tma_load_2d(sQ + b * C::kBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x);
-          if (nb > 0) tma_load_2d(sQ + C::kTileBytes + b * C::kBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x + 128);
+    reg_dealloc<kRegsCtl>();
+    if (warp == 0) {
+      // ============================ scheduler + TMA producer ============================
+      uint32_t qph = 0, ks = 0, kph = 0, islot = 0, iph = 0;
+      while (true) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(p.n_items + 1, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        const int4 it = item < n_items ? __ldg(p.items + item) : make_int4(-1, 0, 0, 0);
+        mbar_wait(&bars.item_empty[islot], iph ^ 1, 16);
+        if (lane == 0) {
+          item_slot[islot] = it;
+          mbar_arrive(&bars.item_full[islot]);  // release: the slot write is visible to the waiting consumers
+        }
+        if (++islot == 2) {
+          islot = 0;
+          iph ^= 1;
+        }
+        if (it.x < 0) break;
+        const int nb = it.y >> 16;
+        const int ng = __ldg(p.ngroups + it.z);
+        const int2* grp = p.groups + size_t(it.z) * p.gcap;
+        mbar_wait(&bars.q_empty, qph ^ 1, 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&bars.q_full, (nb > 0 ? 2u : 1u) * C::kTileBytes);
+          for (int b = 0; b < C::kBlocks; ++b) {
+            tma_load_2d(sQ + b * C::kBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x);
+            if (nb > 0)
+              tma_load_2d(sQ + C::kTileBytes + b * C::kBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x + 128);
+          }
+        }
+        qph ^= 1;
+        const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
+        for (int t = 0; t < T; ++t) {
+          const int gbase = t * kGroupsPerTile;
+          const int ngt = min(kGroupsPerTile, ng - gbase);
+          const int2 gw = lane < ngt ? __ldg(grp + gbase + lane) : make_int2(0, 0);
+          const uint32_t bytes = uint32_t(ngt) * C::kGroupBytes;
+          mbar_wait(&bars.k_empty[ks], kph ^ 1, 2);
+          if (lane == 0) mbar_arrive_expect_tx(&bars.k_full[ks], bytes);
+          __syncwarp();
+          load_kv_tile<D>(kv.k, sK + ks * C::kTileBytes, &bars.k_full[ks], ngt, lane, gw);
+          mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
+          if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], bytes);
+          __syncwarp();
+          load_kv_tile<D>(kv.v, sV + ks * C::kTileBytes, &bars.v_full[ks], ngt, lane, gw);
+          if (++ks == kStages) {
+            ks = 0;
+            kph ^= 1;
+          }
         }
       }
-      qph ^= 1;
-      (void)na;
-      int r = 0, off = 0;
-      const int T = (nkeys + kKTile - 1) / kKTile;
-      for (int t = 0; t < T; ++t) {
-        int rows[4];
-        tile_rows(runs, rc, r, off, t * kKTile, nkeys, lane, rows);
-        mbar_wait(&bars.k_empty[ks], kph ^ 1, 2);
-        if (lane == 0) mbar_arrive_expect_tx(&bars.k_full[ks], C::kTileBytes);
+    } else if (warp == 1) {
+      // ============================ MMA issuer ============================
+      uint32_t qph = 0, ks = 0, kph = 0, vs = 0, vph = 0, islot = 0, iph = 0;
+      uint32_t oeph[2] = {0, 0}, pph[2] = {0, 0};
+      const uint32_t idesc_pv = idesc_bf16_f32(128, D, true);
+      const uint32_t sQa = smem_u32(sQ), sQb = smem_u32(sQ + C::kTileBytes);
+      while (true) {
+        mbar_wait(&bars.item_full[islot], iph, 17);
+        const int4 it = item_slot[islot];
         __syncwarp();
-        uint8_t* dk = sK + ks * C::kTileBytes + lane * 512;
-        for (int b = 0; b < C::kBlocks; ++b)
-          tma_gather4(dk + b * C::kBlockBytes, &mapK, &bars.k_full[ks], 64 * b, rows[0], rows[1], rows[2], rows[3]);
-        mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
-        if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], C::kTileBytes);
+        if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
+        if (++islot == 2) {
+          islot = 0;
+          iph ^= 1;
+        }
+        if (it.x < 0) break;
+        const bool has_b = (it.y >> 16) > 0;
+        const int ng = __ldg(p.ngroups + it.z);
+        const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
+        auto tile_n = [&](int t) { return uint32_t(min(kGroupsPerTile, ng - t * kGroupsPerTile)) * 8u; };
+        auto issue_s = [&](int t, int g, uint32_t kstage) {
+          const uint32_t idesc = idesc_bf16_f32(128, tile_n(t), false);
+          const uint32_t qa = g == 0 ? sQa : sQb;
+          const uint32_t kb = smem_u32(sK + kstage * C::kTileBytes);
+          const uint32_t dcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+            mma_ss(dcol, desc_kmajor_sw128(qa + off), desc_kmajor_sw128(kb + off), idesc, k > 0);
+          }
+        };
+        auto issue_pv = [&](int t, int g, uint32_t vstage) {
+          const int ksteps = int(tile_n(t)) / 16;
+          const uint32_t vb = smem_u32(sV + vstage * C::kTileBytes);
+          const uint32_t pcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
+          const uint32_t dcol = tmem + (g == 0 ? C::kColOa : C::kColOb);
+          for (int k = 0; k < ksteps; ++k)
+            mma_ts(dcol, pcol + 8 * k, desc_mnmajor_sw128(vb + k * 16 * 128, C::kBlockBytes), idesc_pv,
+                   (t > 0 || k > 0) ? 1u : 0u);
+        };
+        mbar_wait(&bars.q_full, qph, 4);
+        qph ^= 1;
+        // prologue: S(0)
+        mbar_wait(&bars.k_full[ks], kph, 5);
+        tc_fence_after();
+        if (lane == 0) {
+          issue_s(0, 0, ks);
+          mma_commit(&bars.s_full[0]);
+          if (has_b) {
+            issue_s(0, 1, ks);
+            mma_commit(&bars.s_full[1]);
+          }
+          mma_commit(&bars.k_empty[ks]);
+          if (T == 1) mma_commit(&bars.q_empty);
+        }
         __syncwarp();
-        uint8_t* dv = sV + ks * C::kTileBytes + lane * 512;
-        for (int b = 0; b < C::kBlocks; ++b)
-          tma_gather4(dv + b * C::kBlockBytes, &mapV, &bars.v_full[ks], 64 * b, rows[0], rows[1], rows[2], rows[3]);
         if (++ks == kStages) {
           ks = 0;
           kph ^= 1;
         }
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    uint32_t qph = 0, ks = 0, kph = 0, vs = 0, vph = 0;
-    uint32_t sph[2] = {0, 0}, oeph[2] = {0, 0};
-    (void)sph;
-    uint32_t pph[2] = {0, 0};
-    const uint32_t idesc_pv = idesc_bf16_f32(128, D, true);
-    const uint32_t sQa = smem_u32(sQ), sQb = smem_u32(sQ + C::kTileBytes);
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int4 it = __ldg(p.items + item);
-      const bool has_b = (it.y >> 16) > 0;
-      const int nkeys = item_keys(p, it);
-      const int T = (nkeys + kKTile - 1) / kKTile;
-      auto issue_s = [&](int t, int g, uint32_t kstage) {
-        const int nvalid = min(kKTile, nkeys - t * kKTile);
-        const uint32_t Nt = (uint32_t(nvalid) + 15u) & ~15u;
-        const uint32_t idesc = idesc_bf16_f32(128, Nt, false);
-        const uint32_t qa = g == 0 ? sQa : sQb;
-        const uint32_t kb = smem_u32(sK + kstage * C::kTileBytes);
-        const uint32_t dcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
-          mma_ss(dcol, desc_kmajor_sw128(qa + off), desc_kmajor_sw128(kb + off), idesc, k > 0);
-        }
-      };
-      auto issue_pv = [&](int t, int g, uint32_t vstage) {
-        const int nvalid = min(kKTile, nkeys - t * kKTile);
-        const int ksteps = (nvalid + 15) / 16;
-        const uint32_t vb = smem_u32(sV + vstage * C::kTileBytes);
-        const uint32_t pcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
-        const uint32_t dcol = tmem + (g == 0 ? C::kColOa : C::kColOb);
-        for (int k = 0; k < ksteps; ++k)
-          mma_ts(dcol, pcol + 8 * k, desc_mnmajor_sw128(vb + k * 16 * 128, C::kBlockBytes), idesc_pv,
-                 (t > 0 || k > 0) ? 1u : 0u);
-      };
-      mbar_wait(&bars.q_full, qph, 4);
-      qph ^= 1;
-      // prologue: S(0)
-      mbar_wait(&bars.k_full[ks], kph, 5);
-      tc_fence_after();
-      if (lane == 0) {
-        issue_s(0, 0, ks);
-        mma_commit(&bars.s_full[0]);
-        if (has_b) {
-          issue_s(0, 1, ks);
-          mma_commit(&bars.s_full[1]);
-        }
-        mma_commit(&bars.k_empty[ks]);
-        if (T == 1) mma_commit(&bars.q_empty);
-      }
-      __syncwarp();
-      if (++ks == kStages) {
-        ks = 0;
-        kph ^= 1;
-      }
-      for (int t = 0; t < T; ++t) {
-        const bool more = t + 1 < T;
-        mbar_wait(&bars.v_full[vs], vph, 6);
-        if (more) mbar_wait(&bars.k_full[ks], kph, 7);
-        // ---- tile a
-        mbar_wait(&bars.p_full[0], pph[0], 8);
-        pph[0] ^= 1;
-        if (t == 0) {
-          mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
-          oeph[0] ^= 1;
-        }
-        tc_fence_after();
-        if (lane == 0) {
-          issue_pv(t, 0, vs);
-          if (more) {
-            issue_s(t + 1, 0, ks);
-            mma_commit(&bars.s_full[0]);
-          } else {
-            mma_commit(&bars.o_full[0]);
-          }
-        }
-        __syncwarp();
-        // ---- tile b
-        if (has_b) {
-          mbar_wait(&bars.p_full[1], pph[1], 10);
-          pph[1] ^= 1;
+        for (int t = 0; t < T; ++t) {
+          const bool more = t + 1 < T;
+          mbar_wait(&bars.v_full[vs], vph, 6);
+          if (more) mbar_wait(&bars.k_full[ks], kph, 7);
+          // ---- tile a
+          mbar_wait(&bars.p_full[0], pph[0], 8);
+          pph[0] ^= 1;
           if (t == 0) {
-            mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
-            oeph[1] ^= 1;
+            mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
+            oeph[0] ^= 1;
           }
           tc_fence_after();
           if (lane == 0) {
-            issue_pv(t, 1, vs);
+            issue_pv(t, 0, vs);
             if (more) {
-              issue_s(t + 1, 1, ks);
-              mma_commit(&bars.s_full[1]);
+              issue_s(t + 1, 0, ks);
+              mma_commit(&bars.s_full[0]);
             } else {
-              mma_commit(&bars.o_full[1]);
+              mma_commit(&bars.o_full[0]);
             }
           }
           __syncwarp();
-        }
-        if (lane == 0) {
-          mma_commit(&bars.v_empty[vs]);
-          if (more) {
-            mma_commit(&bars.k_empty[ks]);
-            if (t + 2 == T) mma_commit(&bars.q_empty);
+          // ---- tile b
+          if (has_b) {
+            mbar_wait(&bars.p_full[1], pph[1], 10);
+            pph[1] ^= 1;
+            if (t == 0) {
+              mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
+              oeph[1] ^= 1;
+            }
+            tc_fence_after();
+            if (lane == 0) {
+              issue_pv(t, 1, vs);
+              if (more) {
+                issue_s(t + 1, 1, ks);
+                mma_commit(&bars.s_full[1]);
+              } else {
+                mma_commit(&bars.o_full[1]);
+              }
+            }
+            __syncwarp();
           }
-        }
-        __syncwarp();
-        if (++vs == kStages) {
-          vs = 0;
-          vph ^= 1;
-        }
-        if (more && ++ks == kStages) {
-          ks = 0;
-          kph ^= 1;
+          if (lane == 0) {
+            mma_commit(&bars.v_empty[vs]);
+            if (more) {
+              mma_commit(&bars.k_empty[ks]);
+              if (t + 2 == T) mma_commit(&bars.q_empty);
+            }
+          }
+          __syncwarp();
+          if (++vs == kStages) {
+            vs = 0;
+            vph ^= 1;
+          }
+          if (more && ++ks == kStages) {
+            ks = 0;
+            kph ^= 1;
+          }
         }
       }
     }
-  }
   } else {
     reg_alloc<kRegsSoftmax>();
     // ============================ softmax warpgroups ============================
@@ -339,16 +332,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_addr + (g == 0 ? C::kColSa : C::kColSb);
     const uint32_t tO = tmem + lane_addr + (g == 0 ? C::kColOa : C::kColOb);
-    uint32_t sph = 0, oph = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int4 it = __ldg(p.items + item);
+    const float sl2 = p.scale_log2;
+    uint32_t sph = 0, oph = 0, islot = 0, iph = 0;
+    while (true) {
+      mbar_wait(&bars.item_full[islot], iph, 18);
+      const int4 it = item_slot[islot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
+      if (++islot == 2) {
+        islot = 0;
+        iph ^= 1;
+      }
+      if (it.x < 0) break;
       const int nrows = g == 0 ? (it.y & 0xFFFF) : (it.y >> 16);
       if (nrows <= 0) continue;
-      const int nkeys = item_keys(p, it);
-      const int T = (nkeys + kKTile - 1) / kKTile;
+      const int ng = __ldg(p.ngroups + it.z);
+      const uint64_t* tw = p.tilew + size_t(it.z) * p.tcap;
+      const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
       float m_used = -INFINITY, l = 0.f;
       for (int t = 0; t < T; ++t) {
-        const int nvalid = min(kKTile, nkeys - t * kKTile);
+        const uint64_t word = __ldg(tw + t);  // 4-bit valid counts of the tile's 16 groups (0 beyond the stream)
         mbar_wait(&bars.s_full[g], sph, 12 + g);
         sph ^= 1;
         tc_fence_after();
@@ -358,20 +361,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, s2);
         tmem_ld32(tS + 96, s3);
         tmem_wait_ld();
-        float mt = -INFINITY;
-        const float sl2 = p.scale_log2;
-        auto scale_mask = [&](uint32_t(&a)[32], int c0) {
+        // row max on the raw scores (scale > 0 preserves order); only tiles with padding rows need the mask
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+        if (word == kFullTileWord) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = (c0 + e < nvalid) ? __uint_as_float(a[e]) * sl2 : -INFINITY;
-            a[e] = __float_as_uint(x);
-            mt = fmaxf(mt, x);
+          for (int e = 0; e < 32; e += 2) {
+            mx0 = fmaxf(mx0, fmaxf(__uint_as_float(s0[e]), __uint_as_float(s1[e])));
+            mx1 = fmaxf(mx1, fmaxf(__uint_as_float(s0[e + 1]), __uint_as_float(s1[e + 1])));
+            mx0 = fmaxf(mx0, fmaxf(__uint_as_float(s2[e]), __uint_as_float(s3[e])));
+            mx1 = fmaxf(mx1, fmaxf(__uint_as_float(s2[e + 1]), __uint_as_float(s3[e + 1])));
           }
-        };
-        scale_mask(s0, 0);
-        scale_mask(s1, 32);
-        scale_mask(s2, 64);
-        scale_mask(s3, 96);
+        } else {
+          auto mask_max = [&](uint32_t(&a)[32], int c0) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int c = c0 + e;
+              const uint32_t nv = uint32_t(word >> (4 * (c >> 3))) & 15u;
+              if (uint32_t(c & 7) >= nv) a[e] = __float_as_uint(-INFINITY);
+              mx0 = fmaxf(mx0, __uint_as_float(a[e]));
+            }
+          };
+          mask_max(s0, 0);
+          mask_max(s1, 32);
+          mask_max(s2, 64);
+          mask_max(s3, 96);
+        }
+        const float mt = fmaxf(mx0, mx1) * sl2;
         if (t == 0) {
           m_used = mt;
         } else if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
@@ -390,14 +405,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_used = m_new;
         }
-        float lsum = 0.f;
+        float lsum0 = 0.f, lsum1 = 0.f;
+        const float neg_m = -m_used;
         auto exp_store = [&](const uint32_t(&a)[32], int c) {
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float p0 = ex2_approx(__uint_as_float(a[2 * e]) - m_used);
-            const float p1 = ex2_approx(__uint_as_float(a[2 * e + 1]) - m_used);
-            lsum += p0 + p1;
+            const float x0 = fmaf(__uint_as_float(a[2 * e]), sl2, neg_m);
+            const float x1 = fmaf(__uint_as_float(a[2 * e + 1]), sl2, neg_m);
+            const bool poly = kPolyStride > 0 && (e % (kPolyStride > 0 ? kPolyStride : 1)) == 0;
+            const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
+            const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
+            lsum0 += p0;
+            lsum1 += p1;
             pk[e] = pack_bf16x2(p0, p1);
           }
           tmem_st16(tS + 16 * c, pk);
@@ -406,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         exp_store(s1, 1);
         exp_store(s2, 2);
         exp_store(s3, 3);
-        l += lsum;
+        l += lsum0 + lsum1;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -453,111 +473,218 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- work-list builder
-constexpr int kBuildThreads = 256;
+constexpr int kBuildThreads = 128;
 
-// per (b,h): runs of selected, non-empty key clusters (ascending j, contiguous ones merged), key counts, and
-// the work items (pairs of 128-row Q tiles) of every non-empty query cluster, in (i, tile) order.
-__global__ void __launch_bounds__(kBuildThreads) k_build(const int32_t* __restrict__ q_off, const int32_t* __restrict__ k_off,
-                                                         const uint8_t* __restrict__ mask, int Nq, int Nk, int Cq,
-                                                         int Ck, int cap, AttnWs ws) {
-  const int bh = blockIdx.x, tid = threadIdx.x;
-  const int per = (Cq + kBuildThreads - 1) / kBuildThreads;
-  const int i0 = min(Cq, tid * per), i1 = min(Cq, i0 + per);
-  const int32_t* qo = q_off + size_t(bh) * (Cq + 1);
-  const int32_t* ko = k_off + size_t(bh) * (Ck + 1);
-  int my_items = 0;
-  for (int i = i0; i < i1; ++i) {
-    const size_t li = size_t(bh) * Cq + i;
-    const uint8_t* mrow = mask + li * Ck;
-    int2* runs = ws.runs + li * Ck;
-    int cnt = 0, keys = 0, cs = -1, ce = -1;
-    for (int j = 0; j < Ck; ++j) {
-      if (!mrow[j]) continue;
-      const int s = __ldg(ko + j), e = __ldg(ko + j + 1);
-      if (e <= s) continue;
-      if (s == ce) {
-        ce = e;
-      } else {
-        if (cs >= 0) {
-          runs[cnt++] = make_int2(int(size_t(bh) * Nk) + cs, ce - cs);
-          keys += ce - cs;
-        }
-        cs = s;
-        ce = e;
-      }
-    }
-    if (cs >= 0) {
-      runs[cnt++] = make_int2(int(size_t(bh) * Nk) + cs, ce - cs);
-      keys += ce - cs;
-    }
-    ws.run_count[li] = cnt;
-    ws.nkeys[li] = keys;
-    const int sq = __ldg(qo + i + 1) - __ldg(qo + i);
-    if (keys > 0) my_items += (sq + kItemRows - 1) / kItemRows;
-  }
-  // exclusive scan of my_items across the block
-  __shared__ int warp_tot[kBuildThreads / 32];
-  int x = my_items;
+// block-wide exclusive scan (kBuildThreads threads, one value each); *total receives the block sum
+__device__ int build_scan(int v, int* total) {
+  __shared__ int wsum[kBuildThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if ((tid & 31) >= o) x += y;
+    if (lane >= o) x += y;
   }
-  if ((tid & 31) == 31) warp_tot[tid >> 5] = x;
+  if (lane == 31) wsum[w] = x;
   __syncthreads();
-  int before = 0, total = 0;
-  for (int w = 0; w < kBuildThreads / 32; ++w) {
-    if (w < (tid >> 5)) before += warp_tot[w];
-    total += warp_tot[w];
+  int before = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < kBuildThreads / 32; ++k) {
+    before += k < w ? wsum[k] : 0;
+    tot += wsum[k];
   }
-  int slot = before + x - my_items;
-  int4* out = ws.items_bh + size_t(bh) * cap;
-  for (int i = i0; i < i1; ++i) {
-    const size_t li = size_t(bh) * Cq + i;
-    const int q0 = __ldg(qo + i), sq = __ldg(qo + i + 1) - q0;
-    if (ws.nkeys[li] <= 0) continue;
-    for (int u = 0; u * kItemRows < sq; ++u) {
-      const int rem = sq - u * kItemRows;
-      const int na = min(kQTile, rem), nb = max(0, min(kQTile, rem - kQTile));
-      out[slot++] = make_int4(int(size_t(bh) * Nq) + q0 + u * kItemRows, na | (nb << 16), int(li), bh);
-    }
-  }
-  if (tid == 0) ws.items_cnt[bh] = total;
+  __syncthreads();
+  *total = tot;
+  return before + x - v;
 }
 
-__global__ void __launch_bounds__(1024) k_flatten(int BH, int cap, AttnWs ws) {
+// One CTA per (b,h,i): the key stream of query cluster i = its selected, non-empty key clusters in ascending j,
+// contiguous clusters merged into runs, runs cut into 8-row groups (the last one partial), the stream padded to an
+// even group count; plus the packed 4-bit valid counts per 16-group tile.  Three block scans (selected clusters,
+// run starts, groups per run) make every step parallel.
+__global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* __restrict__ k_off,
+                                                                 const uint8_t* __restrict__ mask, int Nk, int Cq,
+                                                                 int Ck, AttnWs ws) {
+  extern __shared__ int sbuf[];
+  int* sel_s = sbuf;           // [Ck] start row (within head) of the k-th selected non-empty cluster
+  int* sel_e = sel_s + Ck;     // [Ck] end row
+  int* run_s = sel_e + Ck;     // [Ck] run start
+  int* run_e = run_s + Ck;     // [Ck] run end
+  int* run_g = run_e + Ck;     // [Ck+1] first group of the run
+  __shared__ int n_sel_sh, n_run_sh;
+  const int i = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
+  const size_t li = size_t(bh) * Cq + i;
+  const uint8_t* mrow = mask + li * Ck;
+  const int32_t* ko = k_off + size_t(bh) * (Ck + 1);
+  // 1) compact the selected, non-empty clusters (ascending j)
   int base = 0;
-  for (int bh = 0; bh < BH; ++bh) {
-    const int cnt = ws.items_cnt[bh];
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) ws.items[base + t] = ws.items_bh[size_t(bh) * cap + t];
-    base += cnt;
+  for (int j0 = 0; j0 < Ck; j0 += kBuildThreads) {
+    const int j = j0 + tid;
+    int s = 0, e = 0, f = 0;
+    if (j < Ck && mrow[j]) {
+      s = __ldg(ko + j);
+      e = __ldg(ko + j + 1);
+      f = e > s;
+    }
+    int tot;
+    const int pos = base + build_scan(f, &tot);
+    if (f) {
+      sel_s[pos] = s;
+      sel_e[pos] = e;
+    }
+    base += tot;
   }
-  if (threadIdx.x == 0) *ws.n_items = base;
+  const int nsel = base;
+  __syncthreads();
+  // 2) runs: a selected cluster starts a run unless it begins exactly where the previous one ends
+  base = 0;
+  for (int k0 = 0; k0 < nsel; k0 += kBuildThreads) {
+    const int k = k0 + tid;
+    const int f = (k < nsel) && (k == 0 || sel_s[k] != sel_e[k - 1]);
+    int tot;
+    const int r = base + build_scan(f, &tot);
+    if (f) run_s[r] = sel_s[k];
+    base += tot;
+  }
+  const int nrun = base;
+  __syncthreads();
+  for (int k = tid; k < nsel; k += kBuildThreads) {  // the last cluster of each run writes the run end
+    const bool last = (k == nsel - 1) || (sel_s[k + 1] != sel_e[k]);
+    if (last) {
+      // run index of cluster k = number of run starts at or before k, minus one; recover it by binary search
+      int lo = 0, hi = nrun - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (run_s[mid] <= sel_s[k]) lo = mid; else hi = mid - 1;
+      }
+      run_e[lo] = sel_e[k];
+    }
+  }
+  __syncthreads();
+  // 3) groups per run -> group offsets
+  base = 0;
+  for (int r0 = 0; r0 < nrun; r0 += kBuildThreads) {
+    const int r = r0 + tid;
+    const int gr = r < nrun ? (run_e[r] - run_s[r] + 7) / 8 : 0;
+    int tot;
+    const int g0 = base + build_scan(gr, &tot);
+    if (r < nrun) run_g[r] = g0;
+    base += tot;
+  }
+  const int ng_real = base;
+  const int ng = ng_real + (ng_real & 1);  // even group count: every tile has N = 16 k keys
+  if (tid == 0) {
+    run_g[nrun] = ng_real;
+    ws.ngroups[li] = ng;
+  }
+  __syncthreads();
+  const int rowbase = int(size_t(bh) * Nk);
+  int2* grp = ws.groups + li * ws.gcap;
+  auto group_at = [&](int gi) -> int2 {
+    if (gi >= ng_real) return make_int2(rowbase + run_s[0], 0);  // the padding group: valid rows, all masked
+    int lo = 0, hi = nrun - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (run_g[mid] <= gi) lo = mid; else hi = mid - 1;
+    }
+    const int row = run_s[lo] + 8 * (gi - run_g[lo]);
+    return make_int2(rowbase + row, min(8, run_e[lo] - row));
+  };
+  for (int gi = tid; gi < ng; gi += kBuildThreads) grp[gi] = group_at(gi);
+  uint64_t* tw = ws.tilew + li * ws.tcap;
+  const int ntiles = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
+  for (int t = tid; t < ntiles; t += kBuildThreads) {
+    uint64_t word = 0;
+    for (int q = 0; q < kGroupsPerTile && t * kGroupsPerTile + q < ng; ++q)
+      word |= uint64_t(group_at(t * kGroupsPerTile + q).y) << (4 * q);
+    tw[t] = word;
+  }
+}
+
+// Work items in (b,h)-major, cluster order: ceil(|Q_i| / 256) pairs of 128-row Q tiles per non-empty query cluster
+// with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.
+__global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_off, int BH, int Nq, int Cq,
+                                                AttnWs ws) {
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int total_clusters = BH * Cq;
+  int base = 0;
+  for (int c0 = 0; c0 < total_clusters; c0 += 1024) {
+    const int c = c0 + tid;
+    int n = 0, q0 = 0, sq = 0, bh = 0, i = 0;
+    if (c < total_clusters) {
+      bh = c / Cq;
+      i = c - bh * Cq;
+      q0 = q_off[size_t(bh) * (Cq + 1) + i];
+      sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q0;
+      if (ws.ngroups[c] > 0) n = (sq + kItemRows - 1) / kItemRows;
+    }
+    int x = n;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int k = 0; k < 32; ++k) {
+      before += k < w ? wsum[k] : 0;
+      tot += wsum[k];
+    }
+    __syncthreads();
+    int slot = base + before + x - n;
+    for (int u = 0; u < n; ++u) {
+      const int rem = sq - u * kItemRows;
+      const int na = min(kQTile, rem), nb = max(0, min(kQTile, rem - kQTile));
+      ws.items[slot++] = make_int4(int(size_t(bh) * Nq) + q0 + u * kItemRows, na | (nb << 16), c, bh);
+    }
+    base += tot;
+  }
+  if (tid == 0) {
+    ws.n_items[0] = base;
+    ws.n_items[1] = 0;  // dynamic scheduler counter of the next attention launch
+  }
 }
 
 template <int D>
-cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int Ck, float scale,
+cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
                      const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s) {
-  CUtensorMap mq, mk, mv;
-  if (!make_tmap_bf16(&mq, Qp, uint64_t(BH) * Nq, D, 128) || !make_tmap_bf16(&mk, Kp, uint64_t(BH) * Nk, D, 1) ||
-      !make_tmap_bf16(&mv, Vp, uint64_t(BH) * Nk, D, 1))
-    return cudaErrorInvalidValue;
+  CUtensorMap mq;
+  KVMaps kv;
+  if (!make_tmap_bf16(&mq, Qp, uint64_t(BH) * Nq, D, 128)) return cudaErrorInvalidValue;
+  for (int k = 0; k < kBoxKinds; ++k)
+    if (!make_tmap_bf16(&kv.k[k], Kp, uint64_t(BH) * Nk, D, 8u << k) ||
+        !make_tmap_bf16(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k))
+      return cudaErrorInvalidValue;
   Params p;
   p.items = ws.items;
   p.n_items = ws.n_items;
-  p.runs = ws.runs;
-  p.run_count = ws.run_count;
-  p.nkeys = ws.nkeys;
+  p.groups = ws.groups;
+  p.tilew = ws.tilew;
+  p.ngroups = ws.ngroups;
+  p.gcap = ws.gcap;
+  p.tcap = ws.tcap;
   p.q_perm = q_perm;
   p.O = static_cast<__nv_bfloat16*>(O);
   p.lse = lse;
   p.Nq = Nq;
-  p.Ck = Ck;
   p.scale_log2 = scale * 1.4426950408889634f;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_varblock_attn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes);
-  k_varblock_attn<D><<<sms, kThreads, Cfg<D>::kSmemBytes, s>>>(mq, mk, mv, p);
+  // exp2 split between MUFU and the FMA pipes (env SVG2_EXP_POLY_STRIDE overrides, for measurements)
+  static const int poly = [] {
+    const char* e = getenv("SVG2_EXP_POLY_STRIDE");
+    return e ? atoi(e) : kDefaultPolyStride;
+  }();
+  auto launch = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes);
+    kernel<<<sms, kThreads, Cfg<D>::kSmemBytes, s>>>(mq, kv, p);
+  };
+  if (poly == 2) launch(k_varblock_attn<D, 2>);
+  else if (poly == 4) launch(k_varblock_attn<D, 4>);
+  else if (poly == 8) launch(k_varblock_attn<D, 8>);
+  else launch(k_varblock_attn<D, 0>);
   return cudaGetLastError();
 }
 
@@ -565,9 +692,11 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
 
 cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
                                   int Nq, int Nk, int Cq, int Ck, AttnWs ws, cudaStream_t s) {
-  const int cap = items_cap_per_bh(Nq, Cq);
-  k_build<<<BH, kBuildThreads, 0, s>>>(q_offsets, k_offsets, mask, Nq, Nk, Cq, Ck, cap, ws);
-  k_flatten<<<1, 1024, 0, s>>>(BH, cap, ws);
+  const size_t smem = (5 * size_t(Ck) + 1) * sizeof(int);
+  cudaFuncSetAttribute(k_build_streams, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_build_streams<<<dim3(Cq, BH), kBuildThreads, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, ws);
+  k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, ws);
+  (void)Nq;
   return cudaGetLastError();
 }
 
@@ -575,8 +704,9 @@ cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void
                                       int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
                                       AttnWs ws, cudaStream_t s) {
   (void)Cq;
-  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, Ck, scale, q_perm, O, lse, ws, s);
-  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, Ck, scale, q_perm, O, lse, ws, s);
+  (void)Ck;
+  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s);
+  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s);
 }
 
 }  // namespace svg2
