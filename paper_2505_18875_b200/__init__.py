@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsvg2.so")
+LIB_PATH = os.environ.get("SVG2_LIBRARY", os.path.join(_HERE, "libsvg2.so"))
 
 SVG2_WARM_START = 1
 ENTRY_KMEANS, ENTRY_PERMUTE, ENTRY_SELECT_TOPP, ENTRY_VARBLOCK_ATTENTION, ENTRY_UNPERMUTE, ENTRY_SPARSE_ATTENTION = \

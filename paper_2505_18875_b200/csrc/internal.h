@@ -49,6 +49,7 @@ struct KmeansWs {
   uint16_t* c_hi;     // [BH, Cpad, d] bf16 hi part of the centroids (assign operand)
   uint16_t* c_lo;     // [BH, Cpad, d] bf16 lo part: c - hi
   float* c_norm;      // [BH, Cpad]  ||c||^2 (f32), +inf for padding centroids
+  double* c_sum;      // [BH, C, d]  fp64 cluster sums of the update (kept zero between iterations)
 };
 inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   KmeansWs w;
@@ -58,6 +59,7 @@ inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   w.c_hi = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
   w.c_lo = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
   w.c_norm = c.take<float>(size_t(BH) * cent_pad(C));
+  w.c_sum = c.take<double>(size_t(BH) * C * d);
   return w;
 }
 

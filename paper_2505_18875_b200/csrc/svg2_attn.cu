@@ -42,6 +42,7 @@ constexpr int kRegsCtl = 72, kRegsSoftmax = 216, kRegsLaunch = 168;
 static_assert(128 * kRegsCtl + 256 * kRegsSoftmax <= kRegsLaunch * kThreads, "setmaxnreg budget exceeds launch");
 constexpr int kItemConsumers = 1 + 8;  // MMA warp + 8 softmax warps arrive on item_empty
 constexpr int kDefaultPolyStride = 0;
+constexpr int kDefaultSplitP = 0;
 
 template <int D>
 struct Cfg {
@@ -56,7 +57,7 @@ struct Cfg {
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t s_full[2], p_full[2][2], o_full[2], o_empty[2];  // p_full[tile][half of the keys]
   uint64_t item_full[2], item_empty[2];
 };
 
@@ -76,6 +77,8 @@ struct Params {
   float* lse;
   int Nq;
   float scale_log2;
+  int debug_mode;  // timing experiments only (env SVG2_DEBUG_MODE): 1 = softmax skips max/exp (P = 0)
+  int split_p;     // 1 = P handed to the MMA in two halves (env SVG2_SPLIT_P, default kDefaultSplitP)
 };
 
 // Loads one 16-group tile of the item's key stream into a K or V stage.  Lanes 0..ngt-1 hold one group each; a
@@ -107,6 +110,16 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
   }
 }
 
+// Cycle trace of the first item of CTA 0 (SVG2_DEBUG_MODE=2, measurement only): clock64 per tile and event,
+// printed at kernel exit.  Events: 0/2 MMA saw P of tile a/b, 1/3 MMA finished issuing PV+S for a/b, 4/6 softmax
+// a/b got S, 5/7 softmax a/b handed P over, 8/9 producer issued K/V.
+constexpr int kTraceTiles = 48, kTraceEvents = 10;
+#define TRACE(ev, t)                                                                                      \
+  do {                                                                                                    \
+    if (p.debug_mode == 2 && blockIdx.x == 0 && n_done == 0 && (t) < kTraceTiles && (threadIdx.x & 31) == 0) \
+      trace_buf[(ev)*kTraceTiles + (t)] = clock64();                                                      \
+  } while (0)
+
 // kPolyStride > 0: one pair of elements in every kPolyStride takes exp2 on the FMA pipes (ex2_poly) instead of
 // MUFU, balancing the two units (FA4's partial software exp2).
 template <int D, int kPolyStride>
@@ -121,8 +134,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ Bars bars;
   __shared__ uint32_t tmem_slot;
   __shared__ int4 item_slot[2];
+  __shared__ long long trace_buf[kTraceEvents * kTraceTiles];
+  __shared__ int trace_T;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int n_done = 0;  // items finished by this role (the trace covers the first one)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapQ);
     mbar_init(&bars.q_full, 1);
@@ -135,7 +151,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&bars.s_full[g], 1);
-      mbar_init(&bars.p_full[g], 4);
+      mbar_init(&bars.p_full[g][0], 4);
+      mbar_init(&bars.p_full[g][1], 4);
       mbar_init(&bars.o_full[g], 1);
       mbar_init(&bars.o_empty[g], 4);
       mbar_init(&bars.item_full[g], 1);
@@ -193,15 +210,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive_expect_tx(&bars.k_full[ks], bytes);
           __syncwarp();
           load_kv_tile<D>(kv.k, sK + ks * C::kTileBytes, &bars.k_full[ks], ngt, lane, gw);
+          TRACE(8, t);
           mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
           if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], bytes);
           __syncwarp();
           load_kv_tile<D>(kv.v, sV + ks * C::kTileBytes, &bars.v_full[ks], ngt, lane, gw);
+          TRACE(9, t);
           if (++ks == kStages) {
             ks = 0;
             kph ^= 1;
           }
         }
+        if (n_done == 0 && blockIdx.x == 0 && lane == 0) trace_T = T;
+        ++n_done;
       }
     } else if (warp == 1) {
       // ============================ MMA issuer ============================
@@ -234,12 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_ss(dcol, desc_kmajor_sw128(qa + off), desc_kmajor_sw128(kb + off), idesc, k > 0);
           }
         };
-        auto issue_pv = [&](int t, int g, uint32_t vstage) {
+        // PV over the K-steps [k0, k1) of tile t (16 keys per step); half 0 = steps 0-3, half 1 = steps 4-7
+        auto issue_pv = [&](int t, int g, uint32_t vstage, int half) {
           const int ksteps = int(tile_n(t)) / 16;
+          const int k0 = half == 0 ? 0 : 4, k1 = half == 0 ? min(ksteps, 4) : ksteps;
           const uint32_t vb = smem_u32(sV + vstage * C::kTileBytes);
           const uint32_t pcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
           const uint32_t dcol = tmem + (g == 0 ? C::kColOa : C::kColOb);
-          for (int k = 0; k < ksteps; ++k)
+          for (int k = k0; k < k1; ++k)
             mma_ts(dcol, pcol + 8 * k, desc_mnmajor_sw128(vb + k * 16 * 128, C::kBlockBytes), idesc_pv,
                    (t > 0 || k > 0) ? 1u : 0u);
         };
@@ -268,15 +291,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars.v_full[vs], vph, 6);
           if (more) mbar_wait(&bars.k_full[ks], kph, 7);
           // ---- tile a
-          mbar_wait(&bars.p_full[0], pph[0], 8);
+          if (p.split_p) {
+            mbar_wait(&bars.p_full[0][0], pph[0], 8);
+            if (t == 0) {
+              mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
+              oeph[0] ^= 1;
+            }
+            tc_fence_after();
+            if (lane == 0) issue_pv(t, 0, vs, 0);
+            __syncwarp();
+          }
+          mbar_wait(&bars.p_full[0][1], pph[0], 8);
           pph[0] ^= 1;
-          if (t == 0) {
+          if (!p.split_p && t == 0) {
             mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
             oeph[0] ^= 1;
           }
+          TRACE(0, t);
           tc_fence_after();
           if (lane == 0) {
-            issue_pv(t, 0, vs);
+            if (!p.split_p) issue_pv(t, 0, vs, 0);
+            issue_pv(t, 0, vs, 1);
             if (more) {
               issue_s(t + 1, 0, ks);
               mma_commit(&bars.s_full[0]);
@@ -285,17 +320,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           __syncwarp();
+          TRACE(1, t);
           // ---- tile b
           if (has_b) {
-            mbar_wait(&bars.p_full[1], pph[1], 10);
+            if (p.split_p) {
+              mbar_wait(&bars.p_full[1][0], pph[1], 10);
+              if (t == 0) {
+                mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
+                oeph[1] ^= 1;
+              }
+              tc_fence_after();
+              if (lane == 0) issue_pv(t, 1, vs, 0);
+              __syncwarp();
+            }
+            mbar_wait(&bars.p_full[1][1], pph[1], 10);
             pph[1] ^= 1;
-            if (t == 0) {
+            if (!p.split_p && t == 0) {
               mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
               oeph[1] ^= 1;
             }
+            TRACE(2, t);
             tc_fence_after();
             if (lane == 0) {
-              issue_pv(t, 1, vs);
+              if (!p.split_p) issue_pv(t, 1, vs, 0);
+              issue_pv(t, 1, vs, 1);
               if (more) {
                 issue_s(t + 1, 1, ks);
                 mma_commit(&bars.s_full[1]);
@@ -304,7 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             __syncwarp();
+            TRACE(3, t);
           }
+          if (t + 1 == T) ++n_done;
           if (lane == 0) {
             mma_commit(&bars.v_empty[vs]);
             if (more) {
@@ -354,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t word = __ldg(tw + t);  // 4-bit valid counts of the tile's 16 groups (0 beyond the stream)
         mbar_wait(&bars.s_full[g], sph, 12 + g);
         sph ^= 1;
+        if ((warp & 3) == 0) TRACE(4 + 2 * g, t);
         tc_fence_after();
         uint32_t s0[32], s1[32], s2[32], s3[32];
         tmem_ld32(tS + 0, s0);
@@ -361,6 +412,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, s2);
         tmem_ld32(tS + 96, s3);
         tmem_wait_ld();
+        if (p.debug_mode == 1) {  // timing experiment: MMA/TMA pipeline without the softmax math
+          uint32_t z[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) z[e] = s0[e] & 0u;
+          tmem_st16(tS + 0, z);
+          tmem_st16(tS + 16, z);
+          tmem_st16(tS + 32, z);
+          tmem_st16(tS + 48, z);
+          l = 1.f;
+          m_used = 0.f;
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&bars.p_full[g][0]);
+            mbar_arrive(&bars.p_full[g][1]);
+          }
+          continue;
+        }
         // row max on the raw scores (scale > 0 preserves order); only tiles with padding rows need the mask
         float mx0 = -INFINITY, mx1 = -INFINITY;
         if (word == kFullTileWord) {
@@ -405,32 +475,46 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_used = m_new;
         }
-        float lsum0 = 0.f, lsum1 = 0.f;
-        const float neg_m = -m_used;
+        // p = 2^(s * scale*log2e - m): FFMA2 on pairs, MUFU ex2 per element, FADD2 row sums, bf16x2 packs.
+        // P goes back over S in two halves (keys 0-63, 64-127), each announced on its own barrier so the MMA
+        // warp starts PV on the first half while the second half is being exponentiated.
+        const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m_used, -m_used);
+        uint64_t lsum2 = f2(0.f, 0.f);
         auto exp_store = [&](const uint32_t(&a)[32], int c) {
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float x0 = fmaf(__uint_as_float(a[2 * e]), sl2, neg_m);
-            const float x1 = fmaf(__uint_as_float(a[2 * e + 1]), sl2, neg_m);
+            float x0, x1;
+            f2_split(ffma2(f2(__uint_as_float(a[2 * e]), __uint_as_float(a[2 * e + 1])), sl2x2, negm2), x0, x1);
             const bool poly = kPolyStride > 0 && (e % (kPolyStride > 0 ? kPolyStride : 1)) == 0;
             const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
             const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
-            lsum0 += p0;
-            lsum1 += p1;
+            lsum2 = fadd2(lsum2, f2(p0, p1));
             pk[e] = pack_bf16x2(p0, p1);
           }
           tmem_st16(tS + 16 * c, pk);
         };
         exp_store(s0, 0);
         exp_store(s1, 1);
+        if (p.split_p) {
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars.p_full[g][0]);
+        }
         exp_store(s2, 2);
         exp_store(s3, 3);
-        l += lsum0 + lsum1;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.p_full[g]);
+        if (lane == 0) {
+          if (!p.split_p) mbar_arrive(&bars.p_full[g][0]);
+          mbar_arrive(&bars.p_full[g][1]);
+        }
+        if ((warp & 3) == 0) TRACE(5 + 2 * g, t);
+        float ls0, ls1;
+        f2_split(lsum2, ls0, ls1);
+        l += ls0 + ls1;
       }
       // ---- epilogue: O / l  -> bf16 -> original token order (fused pi_q^T)
       mbar_wait(&bars.o_full[g], oph, 14 + g);
@@ -465,11 +549,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_empty[g]);
+      ++n_done;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
+#ifdef SVG2_TRACE_PRINT
+  if (p.debug_mode == 2 && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = trace_buf[8 * kTraceTiles];
+    printf("svg2 trace: T=%d (cycles relative to the first K issue)\n", trace_T);
+    for (int t = 0; t < min(trace_T, kTraceTiles); ++t) {
+      printf("svg2 trace t=%2d", t);
+      for (int e = 0; e < kTraceEvents; ++e) printf(" %8lld", trace_buf[e * kTraceTiles + t] - t0);
+      printf("\n");
+    }
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- work-list builder
@@ -669,6 +765,16 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
   p.lse = lse;
   p.Nq = Nq;
   p.scale_log2 = scale * 1.4426950408889634f;
+  static const int debug_mode = [] {
+    const char* e = getenv("SVG2_DEBUG_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  p.debug_mode = debug_mode;
+  static const int split_p = [] {
+    const char* e = getenv("SVG2_SPLIT_P");
+    return e ? atoi(e) : kDefaultSplitP;
+  }();
+  p.split_p = split_p;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

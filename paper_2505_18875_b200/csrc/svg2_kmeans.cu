@@ -184,36 +184,63 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// Centroid update, pass 1: each CTA sums a contiguous chunk of kSumRows permuted positions (its rows gathered
+// through perm, 256-byte row reads) and flushes one fp64 partial per cluster the chunk touches with atomicAdd.
+// Sums of bf16 values in fp64 are exact at these magnitudes, so the result does not depend on the order of the
+// atomics: deterministic and bit-identical to a sequential fp64 sum.
+constexpr int kSumRows = 64;
+
 template <int D>
-__global__ void __launch_bounds__(D / 2) k_update(const __nv_bfloat16* __restrict__ X, int N, int C,
-                                                  const int32_t* __restrict__ perm, const int32_t* __restrict__ offsets,
-                                                  float* __restrict__ cent) {
-  const int j = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
-  const int o0 = offsets[size_t(bh) * (C + 1) + j], o1 = offsets[size_t(bh) * (C + 1) + j + 1];
-  if (o1 <= o0) return;  // empty cluster keeps its centroid (R6)
+__global__ void __launch_bounds__(D / 2) k_update_sum(const __nv_bfloat16* __restrict__ X, int N, int C,
+                                                      const int32_t* __restrict__ perm,
+                                                      const int32_t* __restrict__ offsets, double* __restrict__ sum) {
+  const int bh = blockIdx.y, t = threadIdx.x;
+  const int p0 = blockIdx.x * kSumRows, p1 = min(N, p0 + kSumRows);
+  const int32_t* off = offsets + size_t(bh) * (C + 1);
+  // cluster of position p0: last j with off[j] <= p0
+  int lo = 0, hi = C - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(off + mid) <= p0) lo = mid; else hi = mid - 1;
+  }
+  int j = lo, next = __ldg(off + j + 1);
   const __nv_bfloat162* Xb = reinterpret_cast<const __nv_bfloat162*>(X) + size_t(bh) * N * (D / 2);
   const int32_t* pm = perm + size_t(bh) * N;
-  double s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0};
-  int p = o0;
-  for (; p + 4 <= o1; p += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float2 f = __bfloat1622float2(__ldg(Xb + size_t(__ldg(pm + p + u)) * (D / 2) + t));
-      s0[u] += double(f.x);
-      s1[u] += double(f.y);
+  double* sb = sum + size_t(bh) * C * D;
+  double s0 = 0.0, s1 = 0.0;
+  bool any = false;
+  for (int p = p0; p < p1; ++p) {
+    while (p >= next) {  // crossed into the next cluster: flush the partial sum
+      if (any) {
+        atomicAdd(sb + size_t(j) * D + 2 * t, s0);
+        atomicAdd(sb + size_t(j) * D + 2 * t + 1, s1);
+      }
+      s0 = s1 = 0.0;
+      any = false;
+      ++j;
+      next = __ldg(off + j + 1);
     }
-  }
-  for (; p < o1; ++p) {
     const float2 f = __bfloat1622float2(__ldg(Xb + size_t(__ldg(pm + p)) * (D / 2) + t));
-    s0[0] += double(f.x);
-    s1[0] += double(f.y);
+    s0 += double(f.x);
+    s1 += double(f.y);
+    any = true;
   }
-  const double cntd = double(o1 - o0);
-  const double m0 = ((s0[0] + s0[1]) + (s0[2] + s0[3])) / cntd;
-  const double m1 = ((s1[0] + s1[1]) + (s1[2] + s1[3])) / cntd;
-  float* c = cent + (size_t(bh) * C + j) * D;
-  c[2 * t] = float(m0);
-  c[2 * t + 1] = float(m1);
+  if (any) {
+    atomicAdd(sb + size_t(j) * D + 2 * t, s0);
+    atomicAdd(sb + size_t(j) * D + 2 * t + 1, s1);
+  }
+}
+
+// Pass 2: c_j = sum_j / |cluster j| (fp64, rounded to f32); empty clusters keep their centroid (R6).  The sums are
+// zeroed for the next iteration.
+template <int D>
+__global__ void __launch_bounds__(D) k_update_mean(int C, const int32_t* __restrict__ offsets,
+                                                   double* __restrict__ sum, float* __restrict__ cent) {
+  const int j = blockIdx.x, bh = blockIdx.y, k = threadIdx.x;
+  const int cnt = offsets[size_t(bh) * (C + 1) + j + 1] - offsets[size_t(bh) * (C + 1) + j];
+  double* s = sum + (size_t(bh) * C + j) * D + k;
+  if (cnt > 0) cent[(size_t(bh) * C + j) * D + k] = float(*s / double(cnt));
+  *s = 0.0;
 }
 
 template <int D>
@@ -234,6 +261,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
     return cudaErrorInvalidValue;
   cudaFuncSetAttribute(k_assign_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<D>::kSmem);
   if (!warm) k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
+  cudaMemsetAsync(ws.c_sum, 0, size_t(BH) * C * D * sizeof(double), s);
   __nv_bfloat16* hi = reinterpret_cast<__nv_bfloat16*>(ws.c_hi);
   __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
   for (int it = 0; it < iters; ++it) {
@@ -242,14 +270,16 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
         mx, mh, ml, ws.c_norm, N, Cpad, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
-    k_update<D><<<dim3(C, BH), D / 2, 0, s>>>(X, N, C, perm, offsets, cent);
+    k_update_sum<D><<<dim3((N + kSumRows - 1) / kSumRows, BH), D / 2, 0, s>>>(X, N, C, perm, offsets, ws.c_sum);
+    k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, offsets, ws.c_sum, cent);
   }
   return cudaGetLastError();
 }
 
 }  // namespace
 
-int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * (3 + kSortLaunches); }
+// split + assign + sort (3) + sum + mean per iteration, plus the cold init
+int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * (4 + kSortLaunches); }
 
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,

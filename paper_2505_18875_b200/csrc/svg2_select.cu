@@ -13,6 +13,7 @@ namespace svg2 {
 namespace {
 
 constexpr int kSelThreads = 256;
+constexpr int kKChunk = 32;  // centroid columns staged per pass (rows padded to kKChunk + 1 floats)
 
 __device__ __forceinline__ bool before(double wa, int ja, double wb, int jb) {
   return wa > wb || (wa == wb && ja < jb);
@@ -27,7 +28,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
   double* w = reinterpret_cast<double*>(smem);          // [sortN]
   double* crow = w + sortN;                             // [d]
   int* idx = reinterpret_cast<int*>(crow + d);          // [sortN]
-  uint8_t* sel = reinterpret_cast<uint8_t*>(idx + sortN);  // [Ck]
+  int* sks = idx + sortN;                                  // [Ck] key-cluster sizes (staged for the serial walk)
+  uint8_t* sel = reinterpret_cast<uint8_t*>(sks + Ck);     // [Ck]
+  float* stage = reinterpret_cast<float*>(sks + Ck + (Ck + 3) / 4 + 4);  // [kSelThreads][kKChunk + 1]
   __shared__ double red[kSelThreads / 32];
   __shared__ long long keys_sh;
   const int i = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
@@ -35,16 +38,33 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
   const float* ckb = ck + size_t(bh) * Ck * d;
   const int32_t* skb = sk + size_t(bh) * Ck;
   for (int k = tid; k < d; k += kSelThreads) crow[k] = double(cqi[k]);
-  for (int j = tid; j < Ck; j += kSelThreads) sel[j] = 0;
-  __syncthreads();
-  double m = -INFINITY;
   for (int j = tid; j < Ck; j += kSelThreads) {
-    const float* c = ckb + size_t(j) * d;
+    sel[j] = 0;
+    sks[j] = __ldg(skb + j);
+  }
+  __syncthreads();
+  // Eq. 1: the key centroids are staged kSelThreads rows x kKChunk columns at a time through padded shared memory
+  // (coalesced global reads, conflict-free row reads); each thread keeps its own sequential FMA chain over k.
+  double m = -INFINITY;
+  for (int j0 = 0; j0 < Ck; j0 += kSelThreads) {
+    const int j = j0 + tid;
     double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc = fma(crow[k], double(__ldg(c + k)), acc);
-    const double S = scale * acc;
-    w[j] = S;
-    if (__ldg(skb + j) > 0) m = fmax(m, S);
+    for (int k0 = 0; k0 < d; k0 += kKChunk) {
+      __syncthreads();
+      for (int e = tid; e < kSelThreads * kKChunk; e += kSelThreads) {
+        const int r = e / kKChunk, c = e - r * kKChunk;
+        stage[r * (kKChunk + 1) + c] = (j0 + r < Ck) ? __ldg(ckb + size_t(j0 + r) * d + k0 + c) : 0.f;
+      }
+      __syncthreads();
+      const float* srow = stage + tid * (kKChunk + 1);
+#pragma unroll 8
+      for (int k = 0; k < kKChunk; ++k) acc = fma(crow[k0 + k], double(srow[k]), acc);
+    }
+    if (j < Ck) {
+      const double S = scale * acc;
+      w[j] = S;
+      if (sks[j] > 0) m = fmax(m, S);
+    }
   }
   // block max (exact, order-free)
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -113,7 +133,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
         if (wr <= 0.0) break;
         if (!(cum < target)) break;
         sel[idx[r]] = 1;
-        keys += __ldg(skb + idx[r]);
+        keys += sks[idx[r]];
         cum = cum + wr;
       }
       keys_sh = keys;
@@ -136,10 +156,11 @@ cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* 
   int sortN = 1;
   while (sortN < Ck) sortN <<= 1;
   const size_t smem = size_t(sortN) * sizeof(double) + size_t(d) * sizeof(double) + size_t(sortN) * sizeof(int) +
-                      size_t(Ck) + 16;
+                      size_t(Ck) * sizeof(int) + (size_t(Ck) / 4 + 5) * sizeof(int) +
+                      size_t(kSelThreads) * (kKChunk + 1) * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr_set = true;
   }
   if (pairs) cudaMemsetAsync(pairs, 0, size_t(BH) * sizeof(int64_t), s);
