@@ -1,4 +1,4 @@
-// svg2_attn.cu — A9 (+ fused A10): dynamic-block-size sparse attention over the permuted, cluster-contiguous
+// svg2_varblock.cu — A9 (+ fused A10): dynamic-block-size sparse attention over the permuted, cluster-contiguous
 // tokens, written for sm_100a.
 //
 // Work item = two 128-row Q tiles of one query cluster i (contiguous rows of Q' after the permutation) sharing ONE
@@ -9,23 +9,26 @@
 // power-of-two boxes of 8..128 rows, so a tile typically costs 1-3 box loads per 64-column half.  Padding rows of a
 // run's last group are masked in the softmax (a 4-bit valid count per group, packed per tile).
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter):
-//   warp 0      scheduler + TMA producer: fetches the next item, broadcasts it through a 2-slot smem ring, loads
-//               the Q tiles (box loads) and the K/V tiles (box loads) into 2-stage rings
-//   warp 1      MMA issuer (one thread): S = Q K^T (SS, K-major both) into TMEM; O += P V (TS: P read from TMEM,
-//               V MN-major) -- ping-pong order PV_a(t), S_a(t+1), PV_b(t), S_b(t+1)
-//   warp 2      TMEM allocator (512 columns: S_a | S_b | O_a | O_b)
-//   warps 4-7   softmax warpgroup for Q tile a; warps 8-11 for Q tile b.  One thread = one query row = one TMEM
-//               lane: tcgen05.ld S, online softmax in registers (exp2 domain, lazy rescale when the running max
-//               grows by > 8), P (bf16) written back over S with tcgen05.st, O rescaled in TMEM when needed;
-//               epilogue O / l -> bf16 -> global, scattered to original token order through pi_q (fused A10).
+// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter).  The warp
+// scheduler favours high warp ids, so the latency-critical single-thread MMA issuers get the highest ones:
+//   warps 0-3   softmax warpgroup for Q tile a; warps 4-7 for Q tile b.  One thread = one query row = one TMEM
+//               lane (warp w owns lanes 32(w%4)..+31): tcgen05.ld S, online softmax in registers (exp2 domain, lazy
+//               rescale when the running max grows by > 8), P (bf16) written back over S with tcgen05.st, O rescaled
+//               in TMEM when needed; epilogue O / l -> bf16 -> global, scattered to original token order through
+//               pi_q (fused A10).
+//   warp 8      scheduler + TMA producer: fetches the next item, broadcasts it through a 2-slot smem ring, loads the
+//               Q tiles and the K/V tiles (box loads) into 2-stage rings
+//   warp 9      TMEM allocator (512 columns: S_a | S_b | O_a | O_b)
+//   warp 11     MMA issuer (whole warp convergent, elect.sync issues; highest priority), for both Q tiles in turn:
+//               S = Q K^T (SS, K-major both) into TMEM, then per key tile O += P V (TS: P read from TMEM, V MN-major)
+//               followed by the next S, which overwrites P only after the PV that reads it (in-order tensor pipe).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cstdlib>
 #include "internal.h"
 #include "ptx.cuh"
 #include "tmap.h"
-#include <cstdlib>
 
 namespace svg2 {
 namespace {
@@ -36,13 +39,13 @@ constexpr int kGroupsPerTile = kKTile / 8;  // 16
 constexpr int kBoxKinds = 5;                // box heights 8, 16, 32, 64, 128 rows
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: P <= 256 between rescales
 constexpr uint64_t kFullTileWord = 0x8888888888888888ull;
-// setmaxnreg budget: the launch reserves 168 regs x 384 threads; warpgroup 0 (producer / MMA / TMEM) shrinks to
-// 72 and the two softmax warpgroups grow to 216.  The sum must not exceed the reservation or .inc never returns.
-constexpr int kRegsCtl = 72, kRegsSoftmax = 216, kRegsLaunch = 168;
+// setmaxnreg budget: the launch reserves 168 regs x 384 threads; the control warpgroup (warps 8-11) shrinks to 72
+// and the two softmax warpgroups grow to 216.  The sum must not exceed the reservation or .inc never returns.
+constexpr int kRegsCtl = 88, kRegsSoftmax = 208, kRegsLaunch = 168;
 static_assert(128 * kRegsCtl + 256 * kRegsSoftmax <= kRegsLaunch * kThreads, "setmaxnreg budget exceeds launch");
-constexpr int kItemConsumers = 1 + 8;  // MMA warp + 8 softmax warps arrive on item_empty
+constexpr int kWarpProducer = 8, kWarpTmem = 9, kWarpMma = 11;  // warp 10 idle
+constexpr int kItemConsumers = 1 + 8;  // the MMA warp + 8 softmax warps arrive on item_empty
 constexpr int kDefaultPolyStride = 0;
-constexpr int kDefaultSplitP = 0;
 
 template <int D>
 struct Cfg {
@@ -51,13 +54,15 @@ struct Cfg {
   static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;
   static constexpr uint32_t kGroupBytes = 8 * 2 * D;   // 8 rows x D bf16
   static constexpr uint32_t kSmemBytes = (2 + 2 * kStages) * kTileBytes + 1024;
-  static constexpr uint32_t kColSa = 0, kColSb = 128, kColOa = 256, kColOb = 384;
+  // TMEM columns: S of Q tile g at col_s(g) (P aliases it as bf16), O at col_o(g)
+  __host__ __device__ static constexpr uint32_t col_s(int g) { return g ? 128u : 0u; }
+  __host__ __device__ static constexpr uint32_t col_o(int g) { return g ? 384u : 256u; }
 };
 
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], p_full[2][2], o_full[2], o_empty[2];  // p_full[tile][half of the keys]
+  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
   uint64_t item_full[2], item_empty[2];
 };
 
@@ -67,7 +72,7 @@ struct KVMaps {
 
 struct Params {
   const int4* items;
-  int32_t* n_items;  // [0] = count, [1] = dynamic-scheduler counter (zeroed by k_flatten)
+  int32_t* n_items;  // [0] = count, [1] = dynamic-scheduler counter (zeroed by k_items)
   const int2* groups;
   const uint64_t* tilew;
   const int32_t* ngroups;
@@ -77,9 +82,18 @@ struct Params {
   float* lse;
   int Nq;
   float scale_log2;
-  int debug_mode;  // timing experiments only (env SVG2_DEBUG_MODE): 1 = softmax skips max/exp (P = 0)
-  int split_p;     // 1 = P handed to the MMA in two halves (env SVG2_SPLIT_P, default kDefaultSplitP)
+  int debug_mode;  // measurement only (env SVG2_DEBUG_MODE): 1 = softmax skips max/exp (P = 0), 2 = cycle trace
 };
+
+// Cycle trace of the first item of CTA 0 (SVG2_DEBUG_MODE=2 with the SVG2_TRACE_PRINT build, measurement only):
+// clock64 per tile and event, printed at kernel exit.  Events: 0/2 MMA a/b saw P, 1/3 MMA a/b finished issuing
+// PV+S, 4/6 softmax a/b got S, 5/7 softmax a/b handed P over, 8/9 producer issued K/V.
+constexpr int kTraceTiles = 48, kTraceEvents = 10;
+#define TRACE(ev, t)                                                                                      \
+  do {                                                                                                    \
+    if (p.debug_mode == 2 && blockIdx.x == 0 && n_done == 0 && (t) < kTraceTiles && (threadIdx.x & 31) == 0) \
+      trace_buf[(ev)*kTraceTiles + (t)] = clock64();                                                      \
+  } while (0)
 
 // Loads one 16-group tile of the item's key stream into a K or V stage.  Lanes 0..ngt-1 hold one group each; a
 // lane whose group does not continue the previous lane's full group starts a run segment and issues power-of-two
@@ -110,18 +124,8 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
   }
 }
 
-// Cycle trace of the first item of CTA 0 (SVG2_DEBUG_MODE=2, measurement only): clock64 per tile and event,
-// printed at kernel exit.  Events: 0/2 MMA saw P of tile a/b, 1/3 MMA finished issuing PV+S for a/b, 4/6 softmax
-// a/b got S, 5/7 softmax a/b handed P over, 8/9 producer issued K/V.
-constexpr int kTraceTiles = 48, kTraceEvents = 10;
-#define TRACE(ev, t)                                                                                      \
-  do {                                                                                                    \
-    if (p.debug_mode == 2 && blockIdx.x == 0 && n_done == 0 && (t) < kTraceTiles && (threadIdx.x & 31) == 0) \
-      trace_buf[(ev)*kTraceTiles + (t)] = clock64();                                                      \
-  } while (0)
-
 // kPolyStride > 0: one pair of elements in every kPolyStride takes exp2 on the FMA pipes (ex2_poly) instead of
-// MUFU, balancing the two units (FA4's partial software exp2).
+// MUFU (FA4's partial software exp2).
 template <int D, int kPolyStride>
 __global__ void __launch_bounds__(kThreads, 1)
     k_varblock_attn(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ KVMaps kv, const Params p) {
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int n_done = 0;  // items finished by this role (the trace covers the first one)
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpProducer && lane == 0) {
     tma_prefetch_desc(&mapQ);
     mbar_init(&bars.q_full, 1);
     mbar_init(&bars.q_empty, 1);
@@ -151,8 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&bars.s_full[g], 1);
-      mbar_init(&bars.p_full[g][0], 4);
-      mbar_init(&bars.p_full[g][1], 4);
+      mbar_init(&bars.p_full[g], 4);
       mbar_init(&bars.o_full[g], 1);
       mbar_init(&bars.o_empty[g], 4);
       mbar_init(&bars.item_full[g], 1);
@@ -160,16 +163,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(&tmem_slot);
+  if (warp == kWarpTmem) tmem_alloc<512>(&tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const int n_items = __ldg(p.n_items);
 
-  if (warp < 4) {
+  if (warp >= 8) {
     reg_dealloc<kRegsCtl>();
-    if (warp == 0) {
+    if (warp == kWarpProducer) {
       // ============================ scheduler + TMA producer ============================
       uint32_t qph = 0, ks = 0, kph = 0, islot = 0, iph = 0;
       while (true) {
@@ -201,11 +204,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         qph ^= 1;
         const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
+        int2 gw = lane < min(kGroupsPerTile, ng) ? __ldg(grp + lane) : make_int2(0, 0);
         for (int t = 0; t < T; ++t) {
-          const int gbase = t * kGroupsPerTile;
-          const int ngt = min(kGroupsPerTile, ng - gbase);
-          const int2 gw = lane < ngt ? __ldg(grp + gbase + lane) : make_int2(0, 0);
+          const int ngt = min(kGroupsPerTile, ng - t * kGroupsPerTile);
           const uint32_t bytes = uint32_t(ngt) * C::kGroupBytes;
+          // prefetch the next tile's group words while this tile's loads are being issued
+          const int nxt = (t + 1) * kGroupsPerTile + lane;
+          const int2 gw_next = (t + 1 < T && nxt < ng) ? __ldg(grp + nxt) : make_int2(0, 0);
           mbar_wait(&bars.k_empty[ks], kph ^ 1, 2);
           if (lane == 0) mbar_arrive_expect_tx(&bars.k_full[ks], bytes);
           __syncwarp();
@@ -216,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           load_kv_tile<D>(kv.v, sV + ks * C::kTileBytes, &bars.v_full[ks], ngt, lane, gw);
           TRACE(9, t);
+          gw = gw_next;
           if (++ks == kStages) {
             ks = 0;
             kph ^= 1;
@@ -224,12 +230,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (n_done == 0 && blockIdx.x == 0 && lane == 0) trace_T = T;
         ++n_done;
       }
-    } else if (warp == 1) {
+    } else if (warp == kWarpMma) {
       // ============================ MMA issuer ============================
+      // Whole warp runs this code convergently; elect.sync inside the asm picks the issuing lane, so descriptors
+      // stay in uniform registers and the MMAs issue back to back.  Order per key tile t (ping-pong):
+      //   PV_a(t), S_a(t+1) | PV_b(t), S_b(t+1)  -- softmax of tile a overlaps tile b's MMAs and vice versa.
       uint32_t qph = 0, ks = 0, kph = 0, vs = 0, vph = 0, islot = 0, iph = 0;
       uint32_t oeph[2] = {0, 0}, pph[2] = {0, 0};
       const uint32_t idesc_pv = idesc_bf16_f32(128, D, true);
-      const uint32_t sQa = smem_u32(sQ), sQb = smem_u32(sQ + C::kTileBytes);
+      const uint64_t dq0 = desc_kmajor_sw128(smem_u32(sQ)), dq1 = desc_kmajor_sw128(smem_u32(sQ + C::kTileBytes));
+      const uint64_t dk0 = desc_kmajor_sw128(smem_u32(sK)), dk1 = desc_kmajor_sw128(smem_u32(sK + C::kTileBytes));
+      const uint64_t dv0 = desc_mnmajor_sw128(smem_u32(sV), C::kBlockBytes);
+      const uint64_t dv1 = desc_mnmajor_sw128(smem_u32(sV + C::kTileBytes), C::kBlockBytes);
       while (true) {
         mbar_wait(&bars.item_full[islot], iph, 17);
         const int4 it = item_slot[islot];
@@ -246,42 +258,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto tile_n = [&](int t) { return uint32_t(min(kGroupsPerTile, ng - t * kGroupsPerTile)) * 8u; };
         auto issue_s = [&](int t, int g, uint32_t kstage) {
           const uint32_t idesc = idesc_bf16_f32(128, tile_n(t), false);
-          const uint32_t qa = g == 0 ? sQa : sQb;
-          const uint32_t kb = smem_u32(sK + kstage * C::kTileBytes);
-          const uint32_t dcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
+          const uint64_t kd = kstage ? dk1 : dk0, qd = g ? dq1 : dq0;
+          const uint32_t d = tmem + C::col_s(g);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
-            mma_ss(dcol, desc_kmajor_sw128(qa + off), desc_kmajor_sw128(kb + off), idesc, k > 0);
+            const uint64_t off = uint64_t(((k >> 2) * C::kBlockBytes + (k & 3) * 32) >> 4);
+            mma_ss_warp(d, qd + off, kd + off, idesc, k > 0);
           }
         };
-        // PV over the K-steps [k0, k1) of tile t (16 keys per step); half 0 = steps 0-3, half 1 = steps 4-7
-        auto issue_pv = [&](int t, int g, uint32_t vstage, int half) {
+        auto issue_pv = [&](int t, int g, uint32_t vstage) {
           const int ksteps = int(tile_n(t)) / 16;
-          const int k0 = half == 0 ? 0 : 4, k1 = half == 0 ? min(ksteps, 4) : ksteps;
-          const uint32_t vb = smem_u32(sV + vstage * C::kTileBytes);
-          const uint32_t pcol = tmem + (g == 0 ? C::kColSa : C::kColSb);
-          const uint32_t dcol = tmem + (g == 0 ? C::kColOa : C::kColOb);
-          for (int k = k0; k < k1; ++k)
-            mma_ts(dcol, pcol + 8 * k, desc_mnmajor_sw128(vb + k * 16 * 128, C::kBlockBytes), idesc_pv,
-                   (t > 0 || k > 0) ? 1u : 0u);
+          const uint64_t vd = vstage ? dv1 : dv0;
+          const uint32_t ps = tmem + C::col_s(g), d = tmem + C::col_o(g);
+#pragma unroll 1
+          for (int k = 0; k < ksteps; ++k)
+            mma_ts_warp(d, ps + 8 * k, vd + uint64_t((k * 16 * 128) >> 4), idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
         };
         mbar_wait(&bars.q_full, qph, 4);
         qph ^= 1;
         // prologue: S(0)
         mbar_wait(&bars.k_full[ks], kph, 5);
         tc_fence_after();
-        if (lane == 0) {
-          issue_s(0, 0, ks);
-          mma_commit(&bars.s_full[0]);
-          if (has_b) {
-            issue_s(0, 1, ks);
-            mma_commit(&bars.s_full[1]);
-          }
-          mma_commit(&bars.k_empty[ks]);
-          if (T == 1) mma_commit(&bars.q_empty);
+        issue_s(0, 0, ks);
+        mma_commit_warp(&bars.s_full[0]);
+        if (has_b) {
+          issue_s(0, 1, ks);
+          mma_commit_warp(&bars.s_full[1]);
         }
-        __syncwarp();
+        mma_commit_warp(&bars.k_empty[ks]);
+        if (T == 1) mma_commit_warp(&bars.q_empty);
         if (++ks == kStages) {
           ks = 0;
           kph ^= 1;
@@ -290,79 +295,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool more = t + 1 < T;
           mbar_wait(&bars.v_full[vs], vph, 6);
           if (more) mbar_wait(&bars.k_full[ks], kph, 7);
-          // ---- tile a
-          if (p.split_p) {
-            mbar_wait(&bars.p_full[0][0], pph[0], 8);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            if (g == 1 && !has_b) break;
+            mbar_wait(&bars.p_full[g], pph[g], 8 + g);
+            pph[g] ^= 1;
             if (t == 0) {
-              mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
-              oeph[0] ^= 1;
+              mbar_wait(&bars.o_empty[g], oeph[g] ^ 1, 10 + g);
+              oeph[g] ^= 1;
             }
+            TRACE(2 * g, t);
             tc_fence_after();
-            if (lane == 0) issue_pv(t, 0, vs, 0);
-            __syncwarp();
-          }
-          mbar_wait(&bars.p_full[0][1], pph[0], 8);
-          pph[0] ^= 1;
-          if (!p.split_p && t == 0) {
-            mbar_wait(&bars.o_empty[0], oeph[0] ^ 1, 9);
-            oeph[0] ^= 1;
-          }
-          TRACE(0, t);
-          tc_fence_after();
-          if (lane == 0) {
-            if (!p.split_p) issue_pv(t, 0, vs, 0);
-            issue_pv(t, 0, vs, 1);
+            issue_pv(t, g, vs);
             if (more) {
-              issue_s(t + 1, 0, ks);
-              mma_commit(&bars.s_full[0]);
+              issue_s(t + 1, g, ks);
+              mma_commit_warp(&bars.s_full[g]);
             } else {
-              mma_commit(&bars.o_full[0]);
+              mma_commit_warp(&bars.o_full[g]);
             }
+            TRACE(2 * g + 1, t);
           }
-          __syncwarp();
-          TRACE(1, t);
-          // ---- tile b
-          if (has_b) {
-            if (p.split_p) {
-              mbar_wait(&bars.p_full[1][0], pph[1], 10);
-              if (t == 0) {
-                mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
-                oeph[1] ^= 1;
-              }
-              tc_fence_after();
-              if (lane == 0) issue_pv(t, 1, vs, 0);
-              __syncwarp();
-            }
-            mbar_wait(&bars.p_full[1][1], pph[1], 10);
-            pph[1] ^= 1;
-            if (!p.split_p && t == 0) {
-              mbar_wait(&bars.o_empty[1], oeph[1] ^ 1, 11);
-              oeph[1] ^= 1;
-            }
-            TRACE(2, t);
-            tc_fence_after();
-            if (lane == 0) {
-              if (!p.split_p) issue_pv(t, 1, vs, 0);
-              issue_pv(t, 1, vs, 1);
-              if (more) {
-                issue_s(t + 1, 1, ks);
-                mma_commit(&bars.s_full[1]);
-              } else {
-                mma_commit(&bars.o_full[1]);
-              }
-            }
-            __syncwarp();
-            TRACE(3, t);
+          mma_commit_warp(&bars.v_empty[vs]);
+          if (more) {
+            mma_commit_warp(&bars.k_empty[ks]);
+            if (t + 2 == T) mma_commit_warp(&bars.q_empty);
           }
-          if (t + 1 == T) ++n_done;
-          if (lane == 0) {
-            mma_commit(&bars.v_empty[vs]);
-            if (more) {
-              mma_commit(&bars.k_empty[ks]);
-              if (t + 2 == T) mma_commit(&bars.q_empty);
-            }
-          }
-          __syncwarp();
           if (++vs == kStages) {
             vs = 0;
             vph ^= 1;
@@ -372,16 +329,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             kph ^= 1;
           }
         }
+        ++n_done;
       }
     }
   } else {
     reg_alloc<kRegsSoftmax>();
     // ============================ softmax warpgroups ============================
-    const int g = (warp - 4) >> 2;                  // 0: tile a, 1: tile b
+    const int g = warp >> 2;                        // 0: tile a, 1: tile b
     const int rloc = ((warp & 3) << 5) + lane;      // row in the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + (g == 0 ? C::kColSa : C::kColSb);
-    const uint32_t tO = tmem + lane_addr + (g == 0 ? C::kColOa : C::kColOb);
+    const uint32_t tS = tmem + lane_addr + C::col_s(g);
+    const uint32_t tO = tmem + lane_addr + C::col_o(g);
     const float sl2 = p.scale_log2;
     uint32_t sph = 0, oph = 0, islot = 0, iph = 0;
     while (true) {
@@ -412,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, s2);
         tmem_ld32(tS + 96, s3);
         tmem_wait_ld();
-        if (p.debug_mode == 1) {  // timing experiment: MMA/TMA pipeline without the softmax math
+        if (p.debug_mode == 1) {  // measurement: the MMA/TMA pipeline without the softmax math
           uint32_t z[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) z[e] = s0[e] & 0u;
@@ -425,10 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&bars.p_full[g][0]);
-            mbar_arrive(&bars.p_full[g][1]);
-          }
+          if (lane == 0) mbar_arrive(&bars.p_full[g]);
           continue;
         }
         // row max on the raw scores (scale > 0 preserves order); only tiles with padding rows need the mask
@@ -475,9 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_used = m_new;
         }
-        // p = 2^(s * scale*log2e - m): FFMA2 on pairs, MUFU ex2 per element, FADD2 row sums, bf16x2 packs.
-        // P goes back over S in two halves (keys 0-63, 64-127), each announced on its own barrier so the MMA
-        // warp starts PV on the first half while the second half is being exponentiated.
+        // p = 2^(s * scale*log2e - m): FFMA2 on pairs, MUFU ex2 per element, FADD2 row sums, bf16x2 packs
         const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m_used, -m_used);
         uint64_t lsum2 = f2(0.f, 0.f);
         auto exp_store = [&](const uint32_t(&a)[32], int c) {
@@ -496,21 +449,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         exp_store(s0, 0);
         exp_store(s1, 1);
-        if (p.split_p) {
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars.p_full[g][0]);
-        }
         exp_store(s2, 2);
         exp_store(s3, 3);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (!p.split_p) mbar_arrive(&bars.p_full[g][0]);
-          mbar_arrive(&bars.p_full[g][1]);
-        }
+        if (lane == 0) mbar_arrive(&bars.p_full[g]);
         if ((warp & 3) == 0) TRACE(5 + 2 * g, t);
         float ls0, ls1;
         f2_split(lsum2, ls0, ls1);
@@ -554,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<512>(tmem);
+  if (warp == kWarpTmem) tmem_dealloc<512>(tmem);
 #ifdef SVG2_TRACE_PRINT
   if (p.debug_mode == 2 && blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t0 = trace_buf[8 * kTraceTiles];
@@ -607,7 +551,6 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   int* run_s = sel_e + Ck;     // [Ck] run start
   int* run_e = run_s + Ck;     // [Ck] run end
   int* run_g = run_e + Ck;     // [Ck+1] first group of the run
-  __shared__ int n_sel_sh, n_run_sh;
   const int i = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
   const size_t li = size_t(bh) * Cq + i;
   const uint8_t* mrow = mask + li * Ck;
@@ -647,8 +590,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   for (int k = tid; k < nsel; k += kBuildThreads) {  // the last cluster of each run writes the run end
     const bool last = (k == nsel - 1) || (sel_s[k + 1] != sel_e[k]);
     if (last) {
-      // run index of cluster k = number of run starts at or before k, minus one; recover it by binary search
-      int lo = 0, hi = nrun - 1;
+      int lo = 0, hi = nrun - 1;  // the run containing cluster k: last run start <= its start
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (run_s[mid] <= sel_s[k]) lo = mid; else hi = mid - 1;
@@ -707,10 +649,10 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
   int base = 0;
   for (int c0 = 0; c0 < total_clusters; c0 += 1024) {
     const int c = c0 + tid;
-    int n = 0, q0 = 0, sq = 0, bh = 0, i = 0;
+    int n = 0, q0 = 0, sq = 0, bh = 0;
     if (c < total_clusters) {
       bh = c / Cq;
-      i = c - bh * Cq;
+      const int i = c - bh * Cq;
       q0 = q_off[size_t(bh) * (Cq + 1) + i];
       sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q0;
       if (ws.ngroups[c] > 0) n = (sq + kItemRows - 1) / kItemRows;
@@ -770,11 +712,6 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
     return e ? atoi(e) : 0;
   }();
   p.debug_mode = debug_mode;
-  static const int split_p = [] {
-    const char* e = getenv("SVG2_SPLIT_P");
-    return e ? atoi(e) : kDefaultSplitP;
-  }();
-  p.split_p = split_p;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -802,7 +739,6 @@ cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_off
   cudaFuncSetAttribute(k_build_streams, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k_build_streams<<<dim3(Cq, BH), kBuildThreads, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, ws);
   k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, ws);
-  (void)Nq;
   return cudaGetLastError();
 }
 
