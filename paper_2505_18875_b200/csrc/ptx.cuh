@@ -83,6 +83,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int ta
   }
 }
 
+// Warp-uniform wait: the loop condition is a warp vote, so every lane leaves together and ptxas can treat the code
+// after it as convergent (uniform-register operands for tcgen05.mma need no per-lane broadcast/collective wrapper).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if (__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+    if (globaltimer_ns() - t0 > kMbarTimeoutNs) __trap();
+  }
+}
+
+// one arrive per warp, issued by an elected lane (warp-convergent code)
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- proxy fences
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA store)
 __device__ __forceinline__ void fence_async_smem() {

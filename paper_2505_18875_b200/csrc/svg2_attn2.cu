@@ -1,4 +1,4 @@
-// svg2_varblock.cu — A9 (+ fused A10): dynamic-block-size sparse attention over the permuted, cluster-contiguous
+// svg2_attn2.cu — A9 (+ fused A10), design v2 (128-key S tiles, single S/P buffer per Q tile): dynamic-block-size sparse attention over the permuted, cluster-contiguous
 // tokens, written for sm_100a.
 //
 // Work item = two 128-row Q tiles of one query cluster i (contiguous rows of Q' after the permutation) sharing ONE
@@ -32,6 +32,7 @@
 
 namespace svg2 {
 namespace {
+// (internal names shared with svg2_attn3.cu live in this file's anonymous namespace)
 
 constexpr int kThreads = 384;
 constexpr int kStages = 2;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ long long trace_buf[kTraceEvents * kTraceTiles];
   __shared__ int trace_T;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   int n_done = 0;  // items finished by this role (the trace covers the first one)
   if (warp == kWarpProducer && lane == 0) {
     tma_prefetch_desc(&mapQ);
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
   const int n_items = __ldg(p.n_items);
 
   if (warp >= 8) {
@@ -243,15 +244,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dv0 = desc_mnmajor_sw128(smem_u32(sV), C::kBlockBytes);
       const uint64_t dv1 = desc_mnmajor_sw128(smem_u32(sV + C::kTileBytes), C::kBlockBytes);
       while (true) {
-        mbar_wait(&bars.item_full[islot], iph, 17);
+        mbar_wait_warp(&bars.item_full[islot], iph);
         const int4 it = item_slot[islot];
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
+        mbar_arrive_warp(&bars.item_empty[islot]);
         if (++islot == 2) {
           islot = 0;
           iph ^= 1;
         }
-        if (it.x < 0) break;
+        if (__all_sync(0xffffffffu, it.x < 0)) break;
         const bool has_b = (it.y >> 16) > 0;
         const int ng = __ldg(p.ngroups + it.z);
         const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
@@ -274,10 +275,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < ksteps; ++k)
             mma_ts_warp(d, ps + 8 * k, vd + uint64_t((k * 16 * 128) >> 4), idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
         };
-        mbar_wait(&bars.q_full, qph, 4);
+        mbar_wait_warp(&bars.q_full, qph);
         qph ^= 1;
         // prologue: S(0)
-        mbar_wait(&bars.k_full[ks], kph, 5);
+        mbar_wait_warp(&bars.k_full[ks], kph);
         tc_fence_after();
         issue_s(0, 0, ks);
         mma_commit_warp(&bars.s_full[0]);
@@ -293,18 +294,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int t = 0; t < T; ++t) {
           const bool more = t + 1 < T;
-          mbar_wait(&bars.v_full[vs], vph, 6);
-          if (more) mbar_wait(&bars.k_full[ks], kph, 7);
+          mbar_wait_warp(&bars.v_full[vs], vph);
+          if (more) mbar_wait_warp(&bars.k_full[ks], kph);
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             if (g == 1 && !has_b) break;
-            mbar_wait(&bars.p_full[g], pph[g], 8 + g);
+            mbar_wait_warp(&bars.p_full[g], pph[g]);
             pph[g] ^= 1;
             if (t == 0) {
-              mbar_wait(&bars.o_empty[g], oeph[g] ^ 1, 10 + g);
+              mbar_wait_warp(&bars.o_empty[g], oeph[g] ^ 1);
               oeph[g] ^= 1;
             }
-            TRACE(2 * g, t);
             tc_fence_after();
             issue_pv(t, g, vs);
             if (more) {
@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               mma_commit_warp(&bars.o_full[g]);
             }
-            TRACE(2 * g + 1, t);
           }
           mma_commit_warp(&bars.v_empty[vs]);
           if (more) {
@@ -512,178 +511,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 }
 
-// ---------------------------------------------------------------- work-list builder
-constexpr int kBuildThreads = 128;
-
-// block-wide exclusive scan (kBuildThreads threads, one value each); *total receives the block sum
-__device__ int build_scan(int v, int* total) {
-  __shared__ int wsum[kBuildThreads / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[w] = x;
-  __syncthreads();
-  int before = 0, tot = 0;
-#pragma unroll
-  for (int k = 0; k < kBuildThreads / 32; ++k) {
-    before += k < w ? wsum[k] : 0;
-    tot += wsum[k];
-  }
-  __syncthreads();
-  *total = tot;
-  return before + x - v;
-}
-
-// One CTA per (b,h,i): the key stream of query cluster i = its selected, non-empty key clusters in ascending j,
-// contiguous clusters merged into runs, runs cut into 8-row groups (the last one partial), the stream padded to an
-// even group count; plus the packed 4-bit valid counts per 16-group tile.  Three block scans (selected clusters,
-// run starts, groups per run) make every step parallel.
-__global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* __restrict__ k_off,
-                                                                 const uint8_t* __restrict__ mask, int Nk, int Cq,
-                                                                 int Ck, AttnWs ws) {
-  extern __shared__ int sbuf[];
-  int* sel_s = sbuf;           // [Ck] start row (within head) of the k-th selected non-empty cluster
-  int* sel_e = sel_s + Ck;     // [Ck] end row
-  int* run_s = sel_e + Ck;     // [Ck] run start
-  int* run_e = run_s + Ck;     // [Ck] run end
-  int* run_g = run_e + Ck;     // [Ck+1] first group of the run
-  const int i = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
-  const size_t li = size_t(bh) * Cq + i;
-  const uint8_t* mrow = mask + li * Ck;
-  const int32_t* ko = k_off + size_t(bh) * (Ck + 1);
-  // 1) compact the selected, non-empty clusters (ascending j)
-  int base = 0;
-  for (int j0 = 0; j0 < Ck; j0 += kBuildThreads) {
-    const int j = j0 + tid;
-    int s = 0, e = 0, f = 0;
-    if (j < Ck && mrow[j]) {
-      s = __ldg(ko + j);
-      e = __ldg(ko + j + 1);
-      f = e > s;
-    }
-    int tot;
-    const int pos = base + build_scan(f, &tot);
-    if (f) {
-      sel_s[pos] = s;
-      sel_e[pos] = e;
-    }
-    base += tot;
-  }
-  const int nsel = base;
-  __syncthreads();
-  // 2) runs: a selected cluster starts a run unless it begins exactly where the previous one ends
-  base = 0;
-  for (int k0 = 0; k0 < nsel; k0 += kBuildThreads) {
-    const int k = k0 + tid;
-    const int f = (k < nsel) && (k == 0 || sel_s[k] != sel_e[k - 1]);
-    int tot;
-    const int r = base + build_scan(f, &tot);
-    if (f) run_s[r] = sel_s[k];
-    base += tot;
-  }
-  const int nrun = base;
-  __syncthreads();
-  for (int k = tid; k < nsel; k += kBuildThreads) {  // the last cluster of each run writes the run end
-    const bool last = (k == nsel - 1) || (sel_s[k + 1] != sel_e[k]);
-    if (last) {
-      int lo = 0, hi = nrun - 1;  // the run containing cluster k: last run start <= its start
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (run_s[mid] <= sel_s[k]) lo = mid; else hi = mid - 1;
-      }
-      run_e[lo] = sel_e[k];
-    }
-  }
-  __syncthreads();
-  // 3) groups per run -> group offsets
-  base = 0;
-  for (int r0 = 0; r0 < nrun; r0 += kBuildThreads) {
-    const int r = r0 + tid;
-    const int gr = r < nrun ? (run_e[r] - run_s[r] + 7) / 8 : 0;
-    int tot;
-    const int g0 = base + build_scan(gr, &tot);
-    if (r < nrun) run_g[r] = g0;
-    base += tot;
-  }
-  const int ng_real = base;
-  const int ng = ng_real + (ng_real & 1);  // even group count: every tile has N = 16 k keys
-  if (tid == 0) {
-    run_g[nrun] = ng_real;
-    ws.ngroups[li] = ng;
-  }
-  __syncthreads();
-  const int rowbase = int(size_t(bh) * Nk);
-  int2* grp = ws.groups + li * ws.gcap;
-  auto group_at = [&](int gi) -> int2 {
-    if (gi >= ng_real) return make_int2(rowbase + run_s[0], 0);  // the padding group: valid rows, all masked
-    int lo = 0, hi = nrun - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (run_g[mid] <= gi) lo = mid; else hi = mid - 1;
-    }
-    const int row = run_s[lo] + 8 * (gi - run_g[lo]);
-    return make_int2(rowbase + row, min(8, run_e[lo] - row));
-  };
-  for (int gi = tid; gi < ng; gi += kBuildThreads) grp[gi] = group_at(gi);
-  uint64_t* tw = ws.tilew + li * ws.tcap;
-  const int ntiles = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
-  for (int t = tid; t < ntiles; t += kBuildThreads) {
-    uint64_t word = 0;
-    for (int q = 0; q < kGroupsPerTile && t * kGroupsPerTile + q < ng; ++q)
-      word |= uint64_t(group_at(t * kGroupsPerTile + q).y) << (4 * q);
-    tw[t] = word;
-  }
-}
-
-// Work items in (b,h)-major, cluster order: ceil(|Q_i| / 256) pairs of 128-row Q tiles per non-empty query cluster
-// with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.
-__global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_off, int BH, int Nq, int Cq,
-                                                AttnWs ws) {
-  __shared__ int wsum[32];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int total_clusters = BH * Cq;
-  int base = 0;
-  for (int c0 = 0; c0 < total_clusters; c0 += 1024) {
-    const int c = c0 + tid;
-    int n = 0, q0 = 0, sq = 0, bh = 0;
-    if (c < total_clusters) {
-      bh = c / Cq;
-      const int i = c - bh * Cq;
-      q0 = q_off[size_t(bh) * (Cq + 1) + i];
-      sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q0;
-      if (ws.ngroups[c] > 0) n = (sq + kItemRows - 1) / kItemRows;
-    }
-    int x = n;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    int before = 0, tot = 0;
-    for (int k = 0; k < 32; ++k) {
-      before += k < w ? wsum[k] : 0;
-      tot += wsum[k];
-    }
-    __syncthreads();
-    int slot = base + before + x - n;
-    for (int u = 0; u < n; ++u) {
-      const int rem = sq - u * kItemRows;
-      const int na = min(kQTile, rem), nb = max(0, min(kQTile, rem - kQTile));
-      ws.items[slot++] = make_int4(int(size_t(bh) * Nq) + q0 + u * kItemRows, na | (nb << 16), c, bh);
-    }
-    base += tot;
-  }
-  if (tid == 0) {
-    ws.n_items[0] = base;
-    ws.n_items[1] = 0;  // dynamic scheduler counter of the next attention launch
-  }
-}
-
 template <int D>
 cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
                      const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s) {
@@ -733,16 +560,7 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
 
 }  // namespace
 
-cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
-                                  int Nq, int Nk, int Cq, int Ck, AttnWs ws, cudaStream_t s) {
-  const size_t smem = (5 * size_t(Ck) + 1) * sizeof(int);
-  cudaFuncSetAttribute(k_build_streams, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  k_build_streams<<<dim3(Cq, BH), kBuildThreads, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, ws);
-  k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, ws);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
+cudaError_t launch_varblock_attention_v2(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                       int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
                                       AttnWs ws, cudaStream_t s) {
   (void)Cq;

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   __shared__ AsgBars bars;
   __shared__ uint32_t tmem_slot;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int bh = blockIdx.y, row0 = blockIdx.x * kAsgRows;
   const int ntile = (row0 + 128 < N) ? 2 : 1;
   const int nchunks = Cpad / kCentChunk;
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -116,33 +116,32 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(128, kCentChunk, false);
-      mbar_wait(&bars.x_full, 0);
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c & 1;
-        const uint32_t ph = (c >> 1) & 1;
-        mbar_wait(&bars.c_full[s], ph);
-        mbar_wait(&bars.acc_empty[s], ph ^ 1);
-        tc_fence_after();
-        const uint32_t h = smem_u32(sH + s * C::kTileBytes), l = smem_u32(sL + s * C::kTileBytes);
-        for (int t = 0; t < ntile; ++t) {
-          const uint32_t x = smem_u32(sX + t * C::kTileBytes);
-          const uint32_t dcol = tmem + (s * 2 + t) * 128;
+    // whole warp, convergent: elect.sync inside the MMA asm -> back-to-back UTCHMMA on uniform registers
+    const uint32_t idesc = idesc_bf16_f32(128, kCentChunk, false);
+    mbar_wait_warp(&bars.x_full, 0);
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c & 1;
+      const uint32_t ph = (c >> 1) & 1;
+      mbar_wait_warp(&bars.c_full[s], ph);
+      mbar_wait_warp(&bars.acc_empty[s], ph ^ 1);
+      tc_fence_after();
+      const uint32_t h = smem_u32(sH + s * C::kTileBytes), l = smem_u32(sL + s * C::kTileBytes);
+      for (int t = 0; t < ntile; ++t) {
+        const uint32_t x = smem_u32(sX + t * C::kTileBytes);
+        const uint32_t dcol = tmem + (s * 2 + t) * 128;
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
-            mma_ss(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(h + off), idesc, k > 0);
-          }
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
-            mma_ss(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(l + off), idesc, 1u);
-          }
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+          mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(h + off), idesc, k > 0);
         }
-        mma_commit(&bars.c_empty[s]);
-        mma_commit(&bars.acc_full[s]);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+          mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(l + off), idesc, 1u);
+        }
       }
+      mma_commit_warp(&bars.c_empty[s]);
+      mma_commit_warp(&bars.acc_full[s]);
     }
   } else {
     const int t = (warp - 2) >> 2;
