@@ -401,25 +401,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         // row max on the raw scores (scale > 0 preserves order); only steps with padding rows need the mask
-        float mx0 = -INFINITY, mx1 = -INFINITY;
-        if (word == kFullHalfWord) {
+        if (word != kFullHalfWord) {
+          // word is lane-uniform: one uniform test per 8-row group, selects only inside partial groups
+          auto apply_mask = [&](uint32_t(&a)[32], int c0) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            mx0 = fmaxf(mx0, fmaxf(__uint_as_float(s0[e]), __uint_as_float(s1[e])));
-            mx1 = fmaxf(mx1, fmaxf(__uint_as_float(s0[e + 1]), __uint_as_float(s1[e + 1])));
-          }
-        } else {
-          auto mask_max = [&](uint32_t(&a)[32], int c0) {
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t nv = (word >> (4 * ((c0 >> 3) + q))) & 15u;
+              if (nv < 8u) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int c = c0 + e;
-              const uint32_t nv = (word >> (4 * (c >> 3))) & 15u;
-              if (uint32_t(c & 7) >= nv) a[e] = __float_as_uint(-INFINITY);
-              mx0 = fmaxf(mx0, __uint_as_float(a[e]));
+                for (int e = 0; e < 8; ++e)
+                  if (uint32_t(e) >= nv) a[8 * q + e] = __float_as_uint(-INFINITY);
+              }
             }
           };
-          mask_max(s0, 0);
-          mask_max(s1, 32);
+          apply_mask(s0, 0);
+          apply_mask(s1, 32);
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(s0[e]), __uint_as_float(s1[e])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(s0[e + 1]), __uint_as_float(s1[e + 1])));
         }
         const float mt = fmaxf(mx0, mx1) * sl2;
         if (n == 0) {
@@ -766,8 +768,11 @@ cudaError_t launch_varblock_attention_v3(const void* Qp, const void* Kp, const v
 cudaError_t launch_varblock_attention_v2(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                          int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
                                          AttnWs ws, cudaStream_t s);
+cudaError_t launch_varblock_attention_v4(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
+                                         int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
+                                         AttnWs ws, cudaStream_t s);
 
-// Both pipeline designs share the work list and produce identical math; env SVG2_ATTN_VARIANT=2|3 selects one for
+// The pipeline designs share the work list and produce identical math; env SVG2_ATTN_VARIANT=2|3|4 selects one for
 // measurements, kDefaultAttnVariant otherwise.
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                       int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
@@ -778,6 +783,8 @@ cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void
   }();
   if (variant == 2)
     return launch_varblock_attention_v2(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
+  if (variant == 4)
+    return launch_varblock_attention_v4(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
   return launch_varblock_attention_v3(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
 }
 

@@ -225,6 +225,29 @@ def test_p1_equals_dense(svg2, oracle_mod, shape):
     assert (O.float() - ref).abs().max().item() <= MAX_ABS
 
 
+@pytest.mark.parametrize("order", ["increasing", "decreasing", "late_spike"])
+def test_online_softmax_rescale(svg2, oracle_mod, order):
+    """Scores that grow along the key stream force the kernel's lazy O/l rescale (and, on the speculative path, the
+    recompute of an already exponentiated tile); the result must still be the dense softmax (one cluster)."""
+    rng = np.random.default_rng(21)
+    N, d = 2000, 128
+    u = rng.choice([-1.0, 1.0], size=d)
+    a = np.linspace(0.0, 4.0, N)
+    if order == "decreasing":
+        a = a[::-1].copy()
+    elif order == "late_spike":
+        a = np.full(N, 0.5)
+        a[1500] = 6.0
+    q = u[None, :] + 0.3 * rng.standard_normal((N, d))
+    k = a[:, None] * u[None, :]
+    v = rng.standard_normal((N, d))
+    Q, K, V = (to_dev(svg2_synth.f32_to_bf16_bits(x.astype(np.float32)).reshape(1, 1, N, d)) for x in (q, k, v))
+    O, pairs, _ = svg2.sparse_attention(Q, K, V, 1, 1, 1, 0.5)
+    assert int(pairs[0, 0]) == N * N
+    check_attention(O[0, 0], oracle_mod.dense_rows(to_f64(Q)[0, 0], to_f64(K)[0, 0], to_f64(V)[0, 0], f32scale(d)),
+                    order)
+
+
 def test_single_cluster_is_dense(svg2, oracle_mod):
     q, k, v = random_qkv(1, 1, 777, 777, 128, seed=12)
     Q, K, V = to_dev(q), to_dev(k), to_dev(v)
