@@ -11,6 +11,11 @@ constexpr int kMaxClusters = 4096;   // C limit (select_topp sorts a row of Ck i
 constexpr int kQTile = 128;          // query rows per tcgen05 M=128 tile
 constexpr int kKTile = 128;          // keys per S tile (N of the QK^T MMA, K of the PV MMA)
 constexpr int kItemRows = 2 * kQTile;  // one attention work item = two Q tiles of one query cluster
+// Work item int4 = {first flat row of Q', rows_a | rows_b << 16, stream index, bh | flags}.  kItemSplit marks an
+// item with one Q tile and >= 2 key tiles: the v2 kernel gives its even key tiles to one softmax warpgroup and the
+// odd ones to the other and merges the two partial softmax states (other pipelines run it as a one-tile item).
+constexpr int kItemSplit = 1 << 30;
+constexpr int kItemBhMask = kItemSplit - 1;
 
 inline int sort_tiles(int N) { return (N + kSortTile - 1) / kSortTile; }
 inline int items_cap_per_bh(int Nq, int Cq) { return (Nq + kItemRows - 1) / kItemRows + Cq; }

@@ -104,6 +104,10 @@ __device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
 
 // ---------------------------------------------------------------- proxy fences
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA store)
+// named barrier `id` (1..15; 0 is __syncthreads) over `threads` threads (a multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ Bars bars;
   __shared__ uint32_t tmem_slot;
   __shared__ int4 item_slot[2];
+  __shared__ float2 merge_ml[kQTile];  // split items: (m, l) of warpgroup b's rows
   __shared__ long long trace_buf[kTraceEvents * kTraceTiles];
   __shared__ int trace_T;
 
@@ -266,12 +267,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (__all_sync(0xffffffffu, it.x < 0)) break;
         const bool has_b = (it.y >> 16) > 0;
+        const bool split = (it.w & kItemSplit) != 0;  // one Q tile, key tiles dealt alternately to a and b
         const int ng = __ldg(p.ngroups + it.z);
         const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
         auto tile_n = [&](int t) { return uint32_t(min(kGroupsPerTile, ng - t * kGroupsPerTile)) * 8u; };
         auto issue_s = [&](int t, int g, uint32_t kstage) {
           const uint32_t idesc = idesc_bf16_f32(128, tile_n(t), false);
-          const uint64_t kd = kstage ? dk1 : dk0, qd = g ? dq1 : dq0;
+          const uint64_t kd = kstage ? dk1 : dk0, qd = (g && !split) ? dq1 : dq0;
           const uint32_t d = tmem + C::col_s(g);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
@@ -279,16 +281,66 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_ss_warp(d, qd + off, kd + off, idesc, k > 0);
           }
         };
-        auto issue_pv = [&](int t, int g, uint32_t vstage) {
+        auto issue_pv = [&](int t, int g, uint32_t vstage, bool first) {
           const int ksteps = int(tile_n(t)) / 16;
           const uint64_t vd = vstage ? dv1 : dv0;
           const uint32_t ps = tmem + C::col_s(g), d = tmem + C::col_o(g);
 #pragma unroll 1
           for (int k = 0; k < ksteps; ++k)
-            mma_ts_warp(d, ps + 8 * k, vd + uint64_t((k * 16 * 128) >> 4), idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
+            mma_ts_warp(d, ps + 8 * k, vd + uint64_t((k * 16 * 128) >> 4), idesc_pv, (!first || k > 0) ? 1u : 0u);
+        };
+        auto next_k = [&] {
+          if (++ks == kStages) {
+            ks = 0;
+            kph ^= 1;
+          }
         };
         mbar_wait_warp(&bars.q_full, qph);
         qph ^= 1;
+        if (split) {
+          // Lone Q tile with T >= 2 key tiles: tile u goes to softmax warpgroup g = u & 1 (both hold the same Q rows
+          // with their own m, l and O; warpgroup a merges them in the epilogue).  Tile order on the K/V rings is
+          // unchanged.  Chain per warpgroup: PV_g(u) then S_g(u + 2).
+          for (int u = 0; u < 2; ++u) {
+            mbar_wait_warp(&bars.k_full[ks], kph);
+            tc_fence_after();
+            issue_s(u, u, ks);
+            mma_commit_warp(&bars.s_full[u]);
+            mma_commit_warp(&bars.k_empty[ks]);
+            if (u == T - 1) mma_commit_warp(&bars.q_empty);
+            next_k();
+          }
+          for (int u = 0; u < T; ++u) {
+            const int g = u & 1;
+            mbar_wait_warp(&bars.v_full[vs], vph);
+            mbar_wait_warp(&bars.p_full[g], pph[g]);
+            pph[g] ^= 1;
+            if (u < 2) {
+              mbar_wait_warp(&bars.o_empty[g], oeph[g] ^ 1);
+              oeph[g] ^= 1;
+            }
+            tc_fence_after();
+            issue_pv(u, g, vs, u < 2);
+            if (u + 2 < T) {
+              mbar_wait_warp(&bars.k_full[ks], kph);
+              tc_fence_after();
+              issue_s(u + 2, g, ks);
+              mma_commit_warp(&bars.s_full[g]);
+              mma_commit_warp(&bars.k_empty[ks]);
+              if (u + 2 == T - 1) mma_commit_warp(&bars.q_empty);
+              next_k();
+            } else {
+              mma_commit_warp(&bars.o_full[g]);
+            }
+            mma_commit_warp(&bars.v_empty[vs]);
+            if (++vs == kStages) {
+              vs = 0;
+              vph ^= 1;
+            }
+          }
+          ++n_done;
+          continue;
+        }
         // prologue: S(0)
         mbar_wait_warp(&bars.k_full[ks], kph);
         tc_fence_after();
@@ -319,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               oeph[g] ^= 1;
             }
             tc_fence_after();
-            issue_pv(t, g, vs);
+            issue_pv(t, g, vs, t == 0);
             if (more) {
               issue_s(t + 1, g, ks);
               mma_commit_warp(&bars.s_full[g]);
@@ -365,16 +417,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         iph ^= 1;
       }
       if (it.x < 0) break;
-      const int nrows = g == 0 ? (it.y & 0xFFFF) : (it.y >> 16);
+      const bool split = (it.w & kItemSplit) != 0;  // both warpgroups on Q tile a, alternate key tiles
+      const int nrows = (g == 0 || split) ? (it.y & 0xFFFF) : (it.y >> 16);
       if (nrows <= 0) continue;
       const int ng = __ldg(p.ngroups + it.z);
       const uint64_t* tw = p.tilew + size_t(it.z) * p.tcap;
       const int T = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
+      const int t_first = split ? g : 0, t_step = split ? 2 : 1;
       float m_used = -INFINITY, l = 0.f;
-      uint64_t word_next = __ldg(tw);
-      for (int t = 0; t < T; ++t) {
+      uint64_t word_next = __ldg(tw + t_first);
+      for (int t = t_first; t < T; t += t_step) {
         const uint64_t word = word_next;  // 4-bit valid counts of the tile's 16 groups (0 beyond the stream)
-        if (t + 1 < T) word_next = __ldg(tw + t + 1);
+        if (t + t_step < T) word_next = __ldg(tw + t + t_step);
         mbar_wait(&bars.s_full[g], sph, 12 + g);
         sph ^= 1;
         if ((warp & 3) == 0) TRACE(4 + 2 * g, t);
@@ -431,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mx1 = fmaxf(mx1, fmaxf(__uint_as_float(s2[e + 1]), __uint_as_float(s3[e + 1])));
         }
         const float mt = fmaxf(mx0, mx1) * sl2;
-        if (t == 0) {
+        if (t == t_first) {
           m_used = mt;
         } else if (__any_sync(0xffffffffu, mt > m_used + p.rescale_thr)) {
           // warp-uniform branch (tcgen05.ld/st are .sync.aligned); rows whose max did not grow get alpha = 1
@@ -487,11 +541,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars.o_full[g], oph, 14 + g);
       oph ^= 1;
       tc_fence_after();
+      if (split) {
+        // Merge the two partial softmax states of the same rows (flash-decoding style): warpgroup b hands (m, l)
+        // over through shared memory, warpgroup a reads O_a and O_b from TMEM and writes
+        //   O = (2^(m_a-m) O_a + 2^(m_b-m) O_b) / (2^(m_a-m) l_a + 2^(m_b-m) l_b),  m = max(m_a, m_b).
+        // Warpgroup a releases both O accumulators (o_empty counts 4 arrivals, one per warp of a).
+        if (g == 1) merge_ml[rloc] = make_float2(m_used, l);
+        named_bar_sync(1, 256);
+        if (g == 1) {
+          ++n_done;
+          continue;
+        }
+        const float2 mlb = merge_ml[rloc];
+        const float m = fmaxf(m_used, mlb.x);
+        const float wa = ex2_approx(m_used - m), wb = ex2_approx(mlb.x - m);
+        const float lt = l * wa + mlb.y * wb;
+        const float ca = wa / lt, cb = wb / lt;
+        const long long row_flat = (long long)it.x + rloc;
+        long long dst = row_flat;
+        if (rloc < nrows && p.q_perm) dst = (long long)(it.w & kItemBhMask) * p.Nq + __ldg(p.q_perm + row_flat);
+        uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);
+        const uint32_t tOb = tmem + lane_addr + C::col_o(1);
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t oa[32], ob[32];
+          tmem_ld32(tO + 32 * c, oa);
+          tmem_ld32(tOb + 32 * c, ob);
+          tmem_wait_ld();
+          if (rloc < nrows) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float r[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                r[e] = __uint_as_float(oa[8 * v + e]) * ca + __uint_as_float(ob[8 * v + e]) * cb;
+              orow[4 * c + v] = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
+                                           pack_bf16x2(r[6], r[7]));
+            }
+          }
+        }
+        if (rloc < nrows && p.lse) p.lse[dst] = (m + __log2f(lt)) * 0.69314718055994531f;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&bars.o_empty[0]);
+          mbar_arrive(&bars.o_empty[1]);
+        }
+        ++n_done;
+        continue;
+      }
       const float inv_l = 1.f / l;
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
       if (rloc < nrows && p.q_perm) {
-        const long long bh = it.w;
+        const long long bh = it.w & kItemBhMask;
         dst = bh * p.Nq + __ldg(p.q_perm + row_flat);
       }
       uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);

@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
       if (rloc < nrows && p.q_perm) {
-        const long long bh = it.w;
+        const long long bh = it.w & kItemBhMask;
         dst = bh * p.Nq + __ldg(p.q_perm + row_flat);
       }
       uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
 // Work items in (b,h)-major, cluster order: ceil(|Q_i| / 256) pairs of 128-row Q tiles per non-empty query cluster
 // with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.
 __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_off, int BH, int Nq, int Cq,
-                                                AttnWs ws) {
+                                                AttnWs ws, int allow_split) {
   __shared__ int wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int total_clusters = BH * Cq;
@@ -687,7 +687,8 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
     for (int u = 0; u < n; ++u) {
       const int rem = sq - u * kItemRows;
       const int na = min(kQTile, rem), nb = max(0, min(kQTile, rem - kQTile));
-      ws.items[slot++] = make_int4(int(size_t(bh) * Nq) + q0 + u * kItemRows, na | (nb << 16), c, bh);
+      const int split = (allow_split && nb == 0 && ws.ngroups[c] > kKTile / 8) ? kItemSplit : 0;
+      ws.items[slot++] = make_int4(int(size_t(bh) * Nq) + q0 + u * kItemRows, na | (nb << 16), c, bh | split);
     }
     base += tot;
   }
@@ -751,7 +752,11 @@ cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_off
   const size_t smem = (5 * size_t(Ck) + 1) * sizeof(int);
   cudaFuncSetAttribute(k_build_streams, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k_build_streams<<<dim3(Cq, BH), kBuildThreads, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, ws);
-  k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, ws);
+  static const int allow_split = [] {  // env SVG2_SPLIT_ITEMS=0 disables split items (measurements)
+    const char* e = getenv("SVG2_SPLIT_ITEMS");
+    return e ? atoi(e) : 1;
+  }();
+  k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, ws, allow_split);
   return cudaGetLastError();
 }
 

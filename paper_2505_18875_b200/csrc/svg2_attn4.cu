@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
       if (rloc < nrows && p.q_perm) {
-        const long long bh = it.w;
+        const long long bh = it.w & kItemBhMask;
         dst = bh * p.Nq + __ldg(p.q_perm + row_flat);
       }
       uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);

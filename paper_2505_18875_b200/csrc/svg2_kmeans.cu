@@ -12,6 +12,7 @@
 //                      Sums of bf16 values in fp64 are exact at these magnitudes, so the update is order-free and
 //                      bit-identical to the oracle's sequential sum.
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "internal.h"
 #include "ptx.cuh"
 #include "tmap.h"
@@ -183,51 +184,76 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-// Centroid update, pass 1: each CTA sums a contiguous chunk of kSumRows permuted positions (its rows gathered
-// through perm, 256-byte row reads) and flushes one fp64 partial per cluster the chunk touches with atomicAdd.
-// Sums of bf16 values in fp64 are exact at these magnitudes, so the result does not depend on the order of the
-// atomics: deterministic and bit-identical to a sequential fp64 sum.
-constexpr int kSumRows = 64;
+// Centroid update, pass 1: each warp sums a contiguous chunk of kSumRows permuted positions (rows gathered through
+// perm; lane l holds D/32 consecutive columns, so one row is one coalesced D*2-byte read) and flushes one fp64
+// partial per cluster the chunk touches with atomicAdd.  kSumUnroll rows are loaded before any is accumulated, so
+// each warp keeps several row reads in flight (the loop is latency-bound otherwise).  Sums of bf16 values in fp64
+// are exact at these magnitudes, so the result does not depend on the order of the atomics: deterministic and
+// bit-identical to a sequential fp64 sum.
+constexpr int kSumRows = 64, kSumUnroll = 8, kSumWarps = 4;
 
 template <int D>
-__global__ void __launch_bounds__(D / 2) k_update_sum(const __nv_bfloat16* __restrict__ X, int N, int C,
-                                                      const int32_t* __restrict__ perm,
-                                                      const int32_t* __restrict__ offsets, double* __restrict__ sum) {
-  const int bh = blockIdx.y, t = threadIdx.x;
-  const int p0 = blockIdx.x * kSumRows, p1 = min(N, p0 + kSumRows);
+__global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat16* __restrict__ X, int N, int C,
+                                                             const int32_t* __restrict__ perm,
+                                                             const int32_t* __restrict__ offsets,
+                                                             double* __restrict__ sum) {
+  constexpr int kCols = D / 32;  // 4 (d = 128) or 2 (d = 64) bf16 per lane
+  using Vec = typename std::conditional<kCols == 4, uint2, uint32_t>::type;
+  const int bh = blockIdx.y, lane = threadIdx.x & 31;
+  const int p0 = (blockIdx.x * kSumWarps + (threadIdx.x >> 5)) * kSumRows;
+  if (p0 >= N) return;
+  const int p1 = min(N, p0 + kSumRows);
   const int32_t* off = offsets + size_t(bh) * (C + 1);
-  // cluster of position p0: last j with off[j] <= p0
-  int lo = 0, hi = C - 1;
+  int lo = 0, hi = C - 1;  // cluster of position p0: last j with off[j] <= p0
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (__ldg(off + mid) <= p0) lo = mid; else hi = mid - 1;
   }
   int j = lo, next = __ldg(off + j + 1);
-  const __nv_bfloat162* Xb = reinterpret_cast<const __nv_bfloat162*>(X) + size_t(bh) * N * (D / 2);
+  const Vec* Xv = reinterpret_cast<const Vec*>(X) + size_t(bh) * N * 32;  // 32 Vec per row
   const int32_t* pm = perm + size_t(bh) * N;
   double* sb = sum + size_t(bh) * C * D;
-  double s0 = 0.0, s1 = 0.0;
+  double acc[kCols];
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
   bool any = false;
-  for (int p = p0; p < p1; ++p) {
-    while (p >= next) {  // crossed into the next cluster: flush the partial sum
-      if (any) {
-        atomicAdd(sb + size_t(j) * D + 2 * t, s0);
-        atomicAdd(sb + size_t(j) * D + 2 * t + 1, s1);
-      }
-      s0 = s1 = 0.0;
-      any = false;
-      ++j;
-      next = __ldg(off + j + 1);
+  auto flush = [&] {
+    if (any) {
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) atomicAdd(sb + size_t(j) * D + kCols * lane + c, acc[c]);
     }
-    const float2 f = __bfloat1622float2(__ldg(Xb + size_t(__ldg(pm + p)) * (D / 2) + t));
-    s0 += double(f.x);
-    s1 += double(f.y);
-    any = true;
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+    any = false;
+  };
+  for (int pb = p0; pb < p1; pb += kSumUnroll) {
+    const int src_l = pb + (lane & (kSumUnroll - 1)) < p1 ? __ldg(pm + pb + (lane & (kSumUnroll - 1))) : 0;
+    Vec v[kSumUnroll];
+#pragma unroll
+    for (int u = 0; u < kSumUnroll; ++u) {
+      const int src = __shfl_sync(0xffffffffu, src_l, u);
+      if (pb + u < p1) v[u] = __ldg(Xv + size_t(src) * 32 + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < kSumUnroll; ++u) {
+      const int pos = pb + u;
+      if (pos >= p1) break;
+      while (pos >= next) {  // crossed into the next cluster: flush the partial sum
+        flush();
+        ++j;
+        next = __ldg(off + j + 1);
+      }
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+      for (int c = 0; c < kCols / 2; ++c) {
+        const float2 f = __bfloat1622float2(h[c]);
+        acc[2 * c] += double(f.x);
+        acc[2 * c + 1] += double(f.y);
+      }
+      any = true;
+    }
   }
-  if (any) {
-    atomicAdd(sb + size_t(j) * D + 2 * t, s0);
-    atomicAdd(sb + size_t(j) * D + 2 * t + 1, s1);
-  }
+  flush();
 }
 
 // Pass 2: c_j = sum_j / |cluster j| (fp64, rounded to f32); empty clusters keep their centroid (R6).  The sums are
@@ -269,7 +295,8 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
         mx, mh, ml, ws.c_norm, N, Cpad, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
-    k_update_sum<D><<<dim3((N + kSumRows - 1) / kSumRows, BH), D / 2, 0, s>>>(X, N, C, perm, offsets, ws.c_sum);
+    k_update_sum<D><<<dim3((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH), 32 * kSumWarps, 0, s>>>(
+        X, N, C, perm, offsets, ws.c_sum);
     k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, offsets, ws.c_sum, cent);
   }
   return cudaGetLastError();

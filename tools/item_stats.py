@@ -20,6 +20,7 @@ ko = ex["k_offsets"].cpu().numpy().reshape(len(heads), -1)
 mask = ex["mask"].cpu().numpy().reshape(len(heads), wl.Cq, wl.Ck)
 single = pair = 0
 slot_rows = used_rows = 0.0
+periods_pair = periods_single = 0.0
 for h in range(len(heads)):
     qs = np.diff(qo[h])
     ks = np.diff(ko[h])
@@ -30,7 +31,13 @@ for h in range(len(heads)):
         n_items = (tiles + 1) // 2
         pair += tiles // 2
         single += tiles % 2
+        periods_pair += (tiles // 2) * T
+        periods_single += (tiles % 2) * T
         slot_rows += n_items * 256 * T
         used_rows += qs[i] * T
 print(f"{wl.name}: items with two Q tiles {pair}, with one {single} ({single / (pair + single):.1%}); "
       f"row-slot efficiency {used_rows / slot_rows:.1%} (pair items x 256 rows x key tiles)")
+scale = wl.H * wl.B / len(heads)
+print(f"key-tile periods per call (all heads): pair items {periods_pair * scale:.0f}, single-tile items "
+      f"{periods_single * scale:.0f} ({periods_single / (periods_pair + periods_single):.1%}); at 3200 cycles per "
+      f"period, 148 SMs, 1.65 GHz: {(periods_pair + periods_single) * scale * 3200 / 148 / 1.65e6:.1f} ms")
