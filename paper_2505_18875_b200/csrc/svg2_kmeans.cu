@@ -5,8 +5,8 @@
 //   k_centroid_split : c (f32) -> hi = bf16(c), lo = bf16(c - hi), ||c||^2 (f32); padded to 128-centroid chunks
 //   k_assign_tc      : the distance GEMM on tcgen05 — X tile (bf16, exact) x [hi | lo]^T accumulated in fp32 in TMEM
 //                      (K = 2d, so x.c carries ~16 mantissa bits of c), argmin_j ||c_j||^2 - 2 x.c_j read back with
-//                      tcgen05.ld (ties -> lowest j).  256 rows per CTA share every centroid chunk; chunks are
-//                      double-buffered in smem (TMA) and in TMEM (MMA of chunk c+1 overlaps the argmin of chunk c).
+//                      tcgen05.ld (ties -> lowest j).  Persistent (one CTA per SM over 128-row units); X and the
+//                      centroid chunks are double-buffered in smem (TMA), accumulators four-deep in TMEM.
 //   stable sort of the labels (svg2_permute.cu)
 //   k_update         : c_j = (sum of its rows, fp64) / |cluster|, stored f32; empty clusters keep their centroid (R6).
 //                      Sums of bf16 values in fp64 are exact at these magnitudes, so the update is order-free and
@@ -20,8 +20,9 @@
 namespace svg2 {
 namespace {
 
-constexpr int kAsgThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 argmin epilogue (2 row tiles x 4 warps)
-constexpr int kAsgRows = 256;     // rows per CTA (two 128-row M tiles sharing each centroid chunk)
+constexpr int kAsgThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 argmin epilogue (one TMEM lane quarter each)
+constexpr int kAsgRows = 128;     // rows per work unit (one M = 128 tile)
+constexpr int kAccStages = 4;     // TMEM accumulator stages of 128 columns
 
 template <int D>
 struct AsgCfg {
@@ -29,6 +30,7 @@ struct AsgCfg {
   static constexpr uint32_t kBlockBytes = 128 * 128;            // 128 rows x 64 bf16
   static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;  // 128 rows x D bf16
   static constexpr uint32_t kNormBytes = kMaxClusters * 4;
+  // X: 2 buffers | centroid chunk stages: 2 x (hi tile + lo tile) | norms
   static constexpr uint32_t kSmem = 2 * kTileBytes + 4 * kTileBytes + kNormBytes + 1024;
 };
 
@@ -55,43 +57,51 @@ __global__ void __launch_bounds__(D) k_centroid_split(const float* __restrict__ 
 }
 
 struct AsgBars {
-  uint64_t x_full, c_full[2], c_empty[2], acc_full[2], acc_empty[2];
+  uint64_t x_full[2], x_empty[2], c_full[2], c_empty[2], acc_full[kAccStages], acc_empty[kAccStages];
 };
 
+// Persistent assignment: one CTA per SM walks a contiguous range of 128-row work units (row tiles of one (b,h); the
+// range is mostly one head).  Per unit the producer loads X (double-buffered) and streams the centroid chunks (two
+// stages, hi and lo tiles); the MMA warp accumulates X [hi | lo]^T per chunk into one of four TMEM stages; the
+// epilogue warps read each stage back and keep the running argmin.  Loads, MMAs and TMEM reads of consecutive
+// units overlap, and TMEM allocation / barrier setup happen once per CTA instead of once per tile.
 template <int D>
 __global__ void __launch_bounds__(kAsgThreads, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
                 const __grid_constant__ CUtensorMap mapLo, const float* __restrict__ c_norm, int N, int Cpad,
-                int32_t* __restrict__ labels) {
+                int BH, int32_t* __restrict__ labels) {
   using C = AsgCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sX = smem;                       // [2 tiles]
+  uint8_t* sX = smem;                       // [2 buffers]
   uint8_t* sH = smem + 2 * C::kTileBytes;   // [2 stages]
   uint8_t* sL = sH + 2 * C::kTileBytes;     // [2 stages]
-  float* sNorm = reinterpret_cast<float*>(sL + 2 * C::kTileBytes);  // [Cpad]
+  float* sNorm = reinterpret_cast<float*>(sL + 2 * C::kTileBytes);  // [Cpad] of the epilogue's current head
   __shared__ AsgBars bars;
   __shared__ uint32_t tmem_slot;
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int bh = blockIdx.y, row0 = blockIdx.x * kAsgRows;
-  const int ntile = (row0 + 128 < N) ? 2 : 1;
+  const int upb = (N + kAsgRows - 1) / kAsgRows;  // units per (b,h)
+  const long long total = (long long)BH * upb;
+  const int u0 = int(total * blockIdx.x / gridDim.x), u1 = int(total * (blockIdx.x + 1) / gridDim.x);
   const int nchunks = Cpad / kCentChunk;
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&mapX);
     tma_prefetch_desc(&mapHi);
     tma_prefetch_desc(&mapLo);
-    mbar_init(&bars.x_full, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.x_full[s], 1);
+      mbar_init(&bars.x_empty[s], 1);
       mbar_init(&bars.c_full[s], 1);
       mbar_init(&bars.c_empty[s], 1);
+    }
+    for (int s = 0; s < kAccStages; ++s) {
       mbar_init(&bars.acc_full[s], 1);
-      mbar_init(&bars.acc_empty[s], 4 * ntile);
+      mbar_init(&bars.acc_empty[s], 4);
     }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(&tmem_slot);
-  for (int j = threadIdx.x; j < Cpad; j += kAsgThreads) sNorm[j] = __ldg(c_norm + size_t(bh) * Cpad + j);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -99,37 +109,41 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const int xrow = bh * N + row0;
-      mbar_arrive_expect_tx(&bars.x_full, ntile * C::kTileBytes);
-      for (int t = 0; t < ntile; ++t)
+      uint32_t cc = 0;
+      for (int u = u0, i = 0; u < u1; ++u, ++i) {
+        const int bh = u / upb, row0 = (u - bh * upb) * kAsgRows;
+        const int xs = i & 1;
+        mbar_wait(&bars.x_empty[xs], ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars.x_full[xs], C::kTileBytes);
         for (int b = 0; b < C::kBlocks; ++b)
-          tma_load_2d(sX + t * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full, 64 * b, xrow + 128 * t);
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c & 1;
-        const uint32_t ph = (c >> 1) & 1;
-        mbar_wait(&bars.c_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&bars.c_full[s], 2 * C::kTileBytes);
-        const int crow = bh * Cpad + c * kCentChunk;
-        for (int b = 0; b < C::kBlocks; ++b) {
-          tma_load_2d(sH + s * C::kTileBytes + b * C::kBlockBytes, &mapHi, &bars.c_full[s], 64 * b, crow);
-          tma_load_2d(sL + s * C::kTileBytes + b * C::kBlockBytes, &mapLo, &bars.c_full[s], 64 * b, crow);
+          tma_load_2d(sX + xs * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full[xs], 64 * b, bh * N + row0);
+        for (int c = 0; c < nchunks; ++c, ++cc) {
+          const int s = cc & 1;
+          mbar_wait(&bars.c_empty[s], ((cc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars.c_full[s], 2 * C::kTileBytes);
+          const int crow = bh * Cpad + c * kCentChunk;
+          for (int b = 0; b < C::kBlocks; ++b) {
+            tma_load_2d(sH + s * C::kTileBytes + b * C::kBlockBytes, &mapHi, &bars.c_full[s], 64 * b, crow);
+            tma_load_2d(sL + s * C::kTileBytes + b * C::kBlockBytes, &mapLo, &bars.c_full[s], 64 * b, crow);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // whole warp, convergent: elect.sync inside the MMA asm -> back-to-back UTCHMMA on uniform registers
     const uint32_t idesc = idesc_bf16_f32(128, kCentChunk, false);
-    mbar_wait_warp(&bars.x_full, 0);
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c & 1;
-      const uint32_t ph = (c >> 1) & 1;
-      mbar_wait_warp(&bars.c_full[s], ph);
-      mbar_wait_warp(&bars.acc_empty[s], ph ^ 1);
-      tc_fence_after();
-      const uint32_t h = smem_u32(sH + s * C::kTileBytes), l = smem_u32(sL + s * C::kTileBytes);
-      for (int t = 0; t < ntile; ++t) {
-        const uint32_t x = smem_u32(sX + t * C::kTileBytes);
-        const uint32_t dcol = tmem + (s * 2 + t) * 128;
+    uint32_t cc = 0, ac = 0;
+    for (int u = u0, i = 0; u < u1; ++u, ++i) {
+      const int xs = i & 1;
+      mbar_wait_warp(&bars.x_full[xs], (i >> 1) & 1);
+      const uint32_t x = smem_u32(sX + xs * C::kTileBytes);
+      for (int c = 0; c < nchunks; ++c, ++cc, ++ac) {
+        const int s = cc & 1, as = ac % kAccStages;
+        mbar_wait_warp(&bars.c_full[s], (cc >> 1) & 1);
+        mbar_wait_warp(&bars.acc_empty[as], ((ac / kAccStages) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t h = smem_u32(sH + s * C::kTileBytes), l = smem_u32(sL + s * C::kTileBytes);
+        const uint32_t dcol = tmem + as * 128;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
@@ -140,27 +154,34 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
           const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
           mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(l + off), idesc, 1u);
         }
+        mma_commit_warp(&bars.c_empty[s]);
+        mma_commit_warp(&bars.acc_full[as]);
       }
-      mma_commit_warp(&bars.c_empty[s]);
-      mma_commit_warp(&bars.acc_full[s]);
+      mma_commit_warp(&bars.x_empty[xs]);
     }
   } else {
-    const int t = (warp - 2) >> 2;
-    if (t < ntile) {
-      const int quarter = warp & 3;
-      const int row = row0 + t * 128 + quarter * 32 + lane;
-      const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+    const int quarter = warp & 3;  // warps 2..5 -> TMEM lane quarters 2, 3, 0, 1
+    const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+    uint32_t ac = 0;
+    int cur_bh = -1;
+    for (int u = u0; u < u1; ++u) {
+      const int bh = u / upb, row0 = (u - bh * upb) * kAsgRows;
+      if (bh != cur_bh) {  // stage this head's ||c||^2 (all four epilogue warps, named barrier 1)
+        named_bar_sync(1, 128);
+        for (int j = threadIdx.x - 64; j < Cpad; j += 128) sNorm[j] = __ldg(c_norm + size_t(bh) * Cpad + j);
+        named_bar_sync(1, 128);
+        cur_bh = bh;
+      }
       float best = INFINITY;
       int bj = 0;
-      for (int c = 0; c < nchunks; ++c) {
-        const int s = c & 1;
-        const uint32_t ph = (c >> 1) & 1;
-        mbar_wait(&bars.acc_full[s], ph);
+      for (int c = 0; c < nchunks; ++c, ++ac) {
+        const int as = ac % kAccStages;
+        mbar_wait(&bars.acc_full[as], (ac / kAccStages) & 1);
         tc_fence_after();
 #pragma unroll
         for (int q = 0; q < kCentChunk / 32; ++q) {
           uint32_t r[32];
-          tmem_ld32(tmem + lane_addr + (s * 2 + t) * 128 + 32 * q, r);
+          tmem_ld32(tmem + lane_addr + as * 128 + 32 * q, r);
           tmem_wait_ld();
           const int j0 = c * kCentChunk + 32 * q;
 #pragma unroll
@@ -174,8 +195,9 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.acc_empty[s]);
+        if (lane == 0) mbar_arrive(&bars.acc_empty[as]);
       }
+      const int row = row0 + quarter * 32 + lane;
       if (row < N) labels[size_t(bh) * N + row] = bj;
     }
   }
@@ -285,14 +307,18 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
       !make_tmap_bf16(&ml, ws.c_lo, uint64_t(BH) * Cpad, D, 128))
     return cudaErrorInvalidValue;
   cudaFuncSetAttribute(k_assign_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<D>::kSmem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long units = (long long)BH * ((N + kAsgRows - 1) / kAsgRows);
+  const int grid_asg = int(units < sms ? units : sms);  // persistent: one CTA per SM
   if (!warm) k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
   cudaMemsetAsync(ws.c_sum, 0, size_t(BH) * C * D * sizeof(double), s);
   __nv_bfloat16* hi = reinterpret_cast<__nv_bfloat16*>(ws.c_hi);
   __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
   for (int it = 0; it < iters; ++it) {
     k_centroid_split<D><<<dim3(Cpad, BH), D, 0, s>>>(cent, C, Cpad, hi, lo, ws.c_norm);
-    k_assign_tc<D><<<dim3((N + kAsgRows - 1) / kAsgRows, BH), kAsgThreads, AsgCfg<D>::kSmem, s>>>(
-        mx, mh, ml, ws.c_norm, N, Cpad, labels);
+    k_assign_tc<D><<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
     k_update_sum<D><<<dim3((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH), 32 * kSumWarps, 0, s>>>(
