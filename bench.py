@@ -382,6 +382,25 @@ def run_ours(args, wl):
                      "inv_density": 1.0 / density if density > 0 else None,
                      "kernel_speedup_vs_dense": (res[best] / attn_ms) if attn_ms > 0 else None,
                      "paper_bar_0.85_over_density": 0.85 / density if density > 0 else None}
+    # ---- tile-work multiplier: MMA area the kernel executes / algorithmic area, from one debug call
+    # outside the timed region (this rank's heads): Q tiles of 128 rows per query cluster; key stream = runs of
+    # adjacent selected key clusters, each padded to whole 8-row groups, the stream rounded up to 16 keys (DESIGN 6)
+    _, _, dx = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, iters_w, top_p, cq.clone(), ck.clone(), warm=True,
+                                     debug=True)
+    q_off = dx["q_offsets"].cpu().numpy().astype(np.int64).reshape(-1, wl.Cq + 1)
+    k_off = dx["k_offsets"].cpu().numpy().astype(np.int64).reshape(-1, wl.Ck + 1)
+    msk = dx["mask"].cpu().numpy().astype(bool).reshape(-1, wl.Cq, wl.Ck)
+    alg = exe = 0
+    for hh in range(msk.shape[0]):
+        sq, sk = np.diff(q_off[hh]), np.diff(k_off[hh])
+        alg += int((sq * (msk[hh] @ sk)).sum())
+        for i in range(wl.Cq):
+            m = msk[hh, i] & (sk > 0)
+            run = np.cumsum(m & ~np.concatenate(([False], m[:-1]))) * m  # run id per selected cluster, 0 = none
+            run_len = np.bincount(run, weights=sk * m)[1:]
+            stream = np.ceil(np.ceil(run_len / 8).sum() * 8 / 16) * 16
+            exe += int(np.ceil(sq[i] / 128) * 128 * stream)
+    tile_work = exe / alg if alg else None
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_oracle_sample(wl, rows=4096, iters=iters_w, heads=2)
@@ -399,7 +418,7 @@ def run_ours(args, wl):
             "density": density, "ms_per_call": t_use, "ms_per_call_with_stage_events": t_call,
             "stages_ms": stage_ms, "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
             "dense_baseline": dense, "cpu_baseline": cpu, "clocks": clocks.summary(),
-            "attention_executed_tflops": achieved,
+            "attention_executed_tflops": achieved, "tile_work_multiplier": tile_work,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
