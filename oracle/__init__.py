@@ -68,6 +68,11 @@ def _load():
     lib.oracle_attention_rows.argtypes = [_dp, _dp, _dp, i64, i64, i32, _vp, _vp, _vp, i32, dbl,
                                           _vp, i64, _dp, _vp]
     lib.oracle_attention_rows.restype = i32
+    u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+    lib.oracle_philox4x32_10.argtypes = [u32p, u32p, u32p]
+    lib.oracle_philox4x32_10.restype = None
+    lib.oracle_kmeanspp_init.argtypes = [_dp, i64, i32, i32, ctypes.c_uint32, ctypes.c_uint32, _i64p]
+    lib.oracle_kmeanspp_init.restype = i32
     _lib = lib
     return lib
 
@@ -98,6 +103,38 @@ def kmeans(X, C, iters, init=None, return_objective=False):
     if return_objective:
         return labels, cent, sizes, ja, jp
     return labels, cent, sizes
+
+
+def philox4x32_10(ctr, key):
+    """The counter-based generator of DESIGN R25: 4 x uint32 out for a 4 x uint32 counter and 2 x uint32 key."""
+    out = np.empty(4, np.uint32)
+    _load().oracle_philox4x32_10(np.asarray(ctr, np.uint32), np.asarray(key, np.uint32), out)
+    return out
+
+
+def kmeanspp_stream(b, h, H, role):
+    """R23 stream id of one (b, h) and role (0 = Q, 1 = K)."""
+    return 2 * (b * H + h) + role
+
+
+def kmeanspp_init(X, C, seed, stream):
+    """k-means++ cold start (generator R25): the C picked row indices, int64 [C]."""
+    X = _f64(X)
+    N, d = X.shape
+    idx = np.empty(C, np.int64)
+    rc = _load().oracle_kmeanspp_init(X, N, d, C, seed, stream, idx)
+    if rc != 0:
+        raise ValueError(f"oracle_kmeanspp_init: invalid arguments (N={N}, C={C})")
+    return idx
+
+
+def kmeanspp(X, C, iters, seed, stream, return_objective=False):
+    """Cold k-means with the k-means++ init: Lloyd iterations from the picked rows.  Returns labels, centroids,
+    sizes (and J_assign, J_post) like kmeans(), plus the picked indices."""
+    X = _f64(X)
+    idx = kmeanspp_init(X, C, seed, stream)
+    res = kmeans(X, C, iters, init=X[idx], return_objective=return_objective)
+    return (*res, idx)
 
 
 def assign(X, centroids):

@@ -10,6 +10,8 @@
  * Citations are PAPER.md line numbers (Doc B = the paper proper) and the DESIGN.md readings R#.
  *
  *   oracle_kmeans            §4.1 Lloyd k-means on Q or K; §4.3 warm start
+ *   oracle_kmeanspp_init     §4.3 k-means++ cold start (generator fixed by DESIGN R25)
+ *   oracle_philox4x32_10     the counter-based generator of R25 (Salmon et al., SC'11)
  *   oracle_permute           §4.1 pi: cluster-contiguous stable ordering
  *   oracle_select_topp       §4.2 Eq.1, Eq.2, top-p
  *   oracle_attention_rows    §3.1 softmax(QK^T/sqrt d)V restricted to the selected
@@ -103,6 +105,97 @@ int oracle_kmeans(const double* X, int64_t N, int d, int C, int iters, const dou
   }
   free(sums);
   free(dmin);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ k-means++ cold start
+ * The paper initialises cold k-means with k-means++ (Arthur & Vassilvitskii 2007): the first centroid is a uniform
+ * random point, each further centroid is point n with probability proportional to D(x_n), the squared distance to
+ * the nearest centroid chosen so far.  The paper names no generator; DESIGN R25 fixes one so that the GPU and this
+ * oracle pick the same points:
+ *   - random numbers: Philox4x32-10 (Salmon et al., SC'11), key = (seed, stream), counter = (j, 0, 0, 0) for pick j;
+ *     stream = 2 * (b * H + h) + role (role 0 = Q, 1 = K);
+ *   - pick 0: n = floor(out0 * N / 2^32);
+ *   - D(x_n) = sum_k (x_nk - c_k)^2 accumulated in ascending k, every operation rounded (sqdist above);
+ *     after each pick D_n <- min(D_n, D(x_n, new centroid));
+ *   - pick j >= 1: integer weights W_n = floor(D_n / D_ref * 2^32), D_ref = max_n D_n after pick 0 (D only
+ *     decreases, so W_n <= 2^32 and the sum fits 64 bits); r = floor((out0 + 2^32 out1) * sum W / 2^64); the pick
+ *     is the smallest n with W_0 + ... + W_n > r.  If every weight is 0, the pick is floor(out0 * N / 2^32).
+ * Integer weights make the sampling exact and independent of summation order.  Returns 0, or -1 on bad args.
+ */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n1 = (uint32_t)p1;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    const uint32_t n3 = (uint32_t)p0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+int oracle_kmeanspp_init(const double* X, int64_t N, int d, int C, uint32_t seed, uint32_t stream, int64_t* idx) {
+  if (C < 1 || (int64_t)C > N || d < 1 || N > ((int64_t)1 << 31)) return -1;
+  double* D = (double*)malloc(sizeof(double) * (size_t)N);
+  uint64_t* W = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)N);
+  const uint32_t key[2] = {seed, stream};
+  double dref = 0.0;
+  for (int j = 0; j < C; ++j) {
+    const uint32_t ctr[4] = {(uint32_t)j, 0u, 0u, 0u};
+    uint32_t out[4];
+    oracle_philox4x32_10(ctr, key, out);
+    int64_t pick;
+    if (j == 0) {
+      pick = (int64_t)(((uint64_t)out[0] * (uint64_t)N) >> 32);
+    } else {
+      uint64_t total = 0;
+      for (int64_t n = 0; n < N; ++n) {
+        W[n] = dref > 0.0 ? (uint64_t)floor(D[n] / dref * 4294967296.0) : 0u;
+        total += W[n];
+      }
+      if (total == 0) {
+        pick = (int64_t)(((uint64_t)out[0] * (uint64_t)N) >> 32);
+      } else {
+        const uint64_t r64 = (uint64_t)out[0] | ((uint64_t)out[1] << 32);
+        const uint64_t r = (uint64_t)(((unsigned __int128)r64 * total) >> 64);
+        uint64_t run = 0;
+        pick = N - 1;
+        for (int64_t n = 0; n < N; ++n) {
+          run += W[n];
+          if (run > r) {
+            pick = n;
+            break;
+          }
+        }
+      }
+    }
+    idx[j] = pick;
+    const double* c = X + (size_t)pick * d;
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+      const double dn = sqdist(X + (size_t)n * d, c, d);
+      D[n] = (j == 0 || dn < D[n]) ? dn : D[n];
+    }
+    if (j == 0) {
+      for (int64_t n = 0; n < N; ++n) dref = D[n] > dref ? D[n] : dref;
+    }
+  }
+  free(D);
+  free(W);
   return 0;
 }
 
