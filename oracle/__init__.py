@@ -113,7 +113,7 @@ def philox4x32_10(ctr, key):
 
 
 def kmeanspp_stream(b, h, H, role):
-    """R23 stream id of one (b, h) and role (0 = Q, 1 = K)."""
+    """R25 stream id of one (b, h) and role (0 = Q, 1 = K)."""
     return 2 * (b * H + h) + role
 
 
