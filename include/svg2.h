@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SVG2_ABI_VERSION 1
+#define SVG2_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SVG2_API __attribute__((visibility("default")))
@@ -46,7 +46,7 @@ typedef enum {
   SVG2_OK = 0,
   SVG2_ERR_NULL_POINTER = 1,       /* a required pointer is NULL */
   SVG2_ERR_INVALID_SHAPE = 2,      /* B,H,N <= 0, d not in {64,128}, sizes beyond the limits above */
-  SVG2_ERR_INVALID_PARAM = 3,      /* C < 1 or C > N or C > 4096, top_p outside (0,1], iters < 1, bad flags */
+  SVG2_ERR_INVALID_PARAM = 3,      /* C < 1 or C > N or C > 4096, top_p outside (0,1], iters < 1, bad flags, role */
   SVG2_ERR_MISALIGNED = 4,         /* a tensor pointer is not 16-byte aligned (TMA requirement) */
   SVG2_ERR_WORKSPACE_TOO_SMALL = 5,/* ws_bytes < svg2_workspace_size(...) */
   SVG2_ERR_UNSUPPORTED_DEVICE = 6, /* current device is not compute capability 10.0 (sm_100) */
@@ -60,14 +60,20 @@ typedef struct {
 
 /* flags */
 #define SVG2_WARM_START 1u /* k-means starts from the caller's centroids (the centroid cache);
-                              otherwise the deterministic strided cold init c_j = x[floor(j*N/C)] (R2) */
+                              otherwise a cold init: the deterministic strided rows c_j = x[floor(j*N/C)] (R2),
+                              or k-means++ with SVG2_INIT_KMEANSPP */
+#define SVG2_INIT_KMEANSPP 2u /* cold init by k-means++ seeding with the generator of
+                                 DESIGN.md R25: Philox4x32-10 keyed (seed, 2*(b*H+h) + role), role 0 = Q, 1 = K;
+                                 picks reproducible bit for bit.  Ignored with SVG2_WARM_START.  Costs C passes over
+                                 X (the expense the centroid cache avoids). */
 
 typedef struct {
   int32_t Cq, Ck;  /* query / key cluster counts (paper default 100 / 500) */
   int32_t iters;   /* Lloyd iterations, exactly (R3) */
   double top_p;    /* top-p target in (0, 1] */
   float scale;     /* softmax scale; 0 => 1/sqrt(d) */
-  uint32_t flags;  /* SVG2_WARM_START */
+  uint32_t flags;  /* SVG2_WARM_START | SVG2_INIT_KMEANSPP */
+  uint32_t seed;   /* k-means++ generator seed (R25); unused otherwise */
 } svg2_config_t;
 
 /* Optional intermediates of the fused call (device pointers, each NULL or sized as in the layout block above)
@@ -102,10 +108,12 @@ SVG2_API size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dims, const 
  * X [B,H,N,d] bf16.  Per (b,h), `iters` iterations of: assign label_n = argmin_j ||x_n - c_j||^2 (ties -> lowest
  * j), then c_j = mean of its tokens (fp64 sums, stored f32; an empty cluster keeps its centroid, R6).
  * centroids [B,H,C,d] f32: input iff flags & SVG2_WARM_START, always output (exact means of the final labels).
+ * Cold start: strided rows, or k-means++ (flags & SVG2_INIT_KMEANSPP) with generator key (seed, 2*(b*H+h) + role),
+ * role 0 for queries, 1 for keys (R25).
  * labels [B,H,N] out (last assign).  sizes [B,H,C] out.  perm / offsets: optional (NULL) outputs = the stable
  * permutation of the final labels, identical to what svg2_permute would compute. */
 SVG2_API svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C, int32_t iters,
-                          uint32_t flags, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
+                          uint32_t flags, uint32_t seed, int32_t role, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
                           int32_t* offsets, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- A3, A4, A6: semantic-aware permutation.

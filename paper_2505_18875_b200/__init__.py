@@ -20,6 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SVG2_LIBRARY", os.path.join(_HERE, "libsvg2.so"))
 
 SVG2_WARM_START = 1
+SVG2_INIT_KMEANSPP = 2  # cold init by k-means++ seeding (generator DESIGN R25)
 ENTRY_KMEANS, ENTRY_PERMUTE, ENTRY_SELECT_TOPP, ENTRY_VARBLOCK_ATTENTION, ENTRY_UNPERMUTE, ENTRY_SPARSE_ATTENTION = \
     range(6)
 STATUS = ["SVG2_OK", "SVG2_ERR_NULL_POINTER", "SVG2_ERR_INVALID_SHAPE", "SVG2_ERR_INVALID_PARAM",
@@ -44,7 +45,7 @@ class Dims(ctypes.Structure):
 
 class Config(ctypes.Structure):
     _fields_ = [("Cq", ctypes.c_int32), ("Ck", ctypes.c_int32), ("iters", ctypes.c_int32), ("top_p", ctypes.c_double),
-                ("scale", ctypes.c_float), ("flags", ctypes.c_uint32)]
+                ("scale", ctypes.c_float), ("flags", ctypes.c_uint32), ("seed", ctypes.c_uint32)]
 
 
 class Debug(ctypes.Structure):
@@ -71,7 +72,7 @@ def load_library(path: str = LIB_PATH):
     lib.svg2_abi_version.restype = ctypes.c_int
     lib.svg2_workspace_size.argtypes = [ctypes.c_int, Dims, ctypes.POINTER(Config)]
     lib.svg2_workspace_size.restype = sz
-    lib.svg2_kmeans.argtypes = [vp, i32, i32, i32, i32, i32, i32, u32, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.svg2_kmeans.argtypes = [vp, i32, i32, i32, i32, i32, i32, u32, u32, i32, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_permute.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_select_topp.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, ctypes.c_float, ctypes.c_double, vp,
                                      vp, vp]
@@ -129,13 +130,24 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 def workspace_size(entry: int, B: int, H: int, Nq: int, Nk: int, d: int, Cq: int, Ck: int = 1, iters: int = 1,
                    top_p: float = 1.0) -> int:
     lib = load_library()
-    cfg = Config(Cq, Ck, iters, top_p, 0.0, 0)
+    cfg = Config(Cq, Ck, iters, top_p, 0.0, 0, 0)
     return int(lib.svg2_workspace_size(entry, Dims(B, H, Nq, Nk, d), ctypes.byref(cfg)))
 
 
-def kmeans(X: torch.Tensor, C: int, iters: int, centroids: torch.Tensor | None = None, return_perm: bool = False):
+def _cold_flags(init: str) -> int:
+    if init == "strided":
+        return 0
+    if init == "kmeans++":
+        return SVG2_INIT_KMEANSPP
+    raise ValueError(f"init must be 'strided' or 'kmeans++', not {init!r}")
+
+
+def kmeans(X: torch.Tensor, C: int, iters: int, centroids: torch.Tensor | None = None, return_perm: bool = False,
+           init: str = "strided", seed: int = 0, role: int = 0):
     """Lloyd k-means per (b,h) of X [B,H,N,d] bf16.  Warm start iff `centroids` ([B,H,C,d] f32) is given; it is
-    updated in place.  Returns (labels, sizes, centroids[, perm, offsets])."""
+    updated in place.  Cold start: init="strided" (rows floor(jN/C), R2) or "kmeans++" with the
+    generator key (seed, 2*(b*H+h) + role), role 0 = queries, 1 = keys (R25).
+    Returns (labels, sizes, centroids[, perm, offsets])."""
     lib = load_library()
     _need(X, torch.bfloat16, "X", 4)
     B, H, N, d = X.shape
@@ -150,7 +162,8 @@ def kmeans(X: torch.Tensor, C: int, iters: int, centroids: torch.Tensor | None =
     offsets = torch.empty(B, H, C + 1, dtype=torch.int32, device=X.device) if return_perm else None
     nbytes = workspace_size(ENTRY_KMEANS, B, H, N, N, d, C, iters=iters)
     ws = _workspace(max(nbytes, 256), X.device)
-    _check("svg2_kmeans", lib.svg2_kmeans(_p(X), B, H, N, d, C, iters, SVG2_WARM_START if warm else 0, _p(centroids),
+    flags = SVG2_WARM_START if warm else _cold_flags(init)
+    _check("svg2_kmeans", lib.svg2_kmeans(_p(X), B, H, N, d, C, iters, flags, seed, role, _p(centroids),
                                           _p(labels), _p(sizes), _p(perm), _p(offsets), _p(ws), ws.numel(),
                                           _stream()))
     if return_perm:
@@ -231,16 +244,18 @@ def unpermute(Op, perm):
     return O
 
 
-def launch_count(B, H, Nq, Nk, d, Cq, Ck, iters, top_p, warm) -> int:
+def launch_count(B, H, Nq, Nk, d, Cq, Ck, iters, top_p, warm, init: str = "strided") -> int:
     lib = load_library()
-    cfg = Config(Cq, Ck, iters, top_p, 0.0, SVG2_WARM_START if warm else 0)
+    cfg = Config(Cq, Ck, iters, top_p, 0.0, SVG2_WARM_START if warm else _cold_flags(init), 0)
     return int(lib.svg2_sparse_attention_launch_count(Dims(B, H, Nq, Nk, d), ctypes.byref(cfg)))
 
 
 def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_centroids=None, k_centroids=None,
-                     warm: bool = False, scale: float = 0.0, debug: bool = False, events=None, out=None):
+                     warm: bool = False, scale: float = 0.0, debug: bool = False, events=None, out=None,
+                     init: str = "strided", seed: int = 0):
     """The fused SVG2 call.  Q, K, V [B,H,N,d] bf16 CUDA.  q_centroids [B,H,Cq,d] / k_centroids [B,H,Ck,d] f32 are
-    the centroid caches (read iff warm, always written).  Returns (O, selected_pairs, extras) where extras holds
+    the centroid caches (read iff warm, always written).  Cold calls start k-means from `init` ("strided" or
+    "kmeans++" with `seed`, R25).  Returns (O, selected_pairs, extras) where extras holds
     the centroids and, if debug, the intermediates (labels, perms, offsets, mask)."""
     lib = load_library()
     for t, n in ((Q, "Q"), (K, "K"), (V, "V")):
@@ -258,7 +273,7 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
     _need(k_centroids, torch.float32, "k_centroids", 4)
     O = out if out is not None else torch.empty_like(Q)
     pairs = torch.empty(B, H, dtype=torch.int64, device=dev)
-    cfg = Config(Cq, Ck, iters, top_p, scale, SVG2_WARM_START if warm else 0)
+    cfg = Config(Cq, Ck, iters, top_p, scale, SVG2_WARM_START if warm else _cold_flags(init), seed)
     dims = Dims(B, H, Nq, Nk, d)
     # 0 = invalid arguments: still call the ABI so the caller gets its precise status code
     nbytes = int(lib.svg2_workspace_size(ENTRY_SPARSE_ATTENTION, dims, ctypes.byref(cfg)))

@@ -55,7 +55,10 @@ struct KmeansWs {
   uint16_t* c_lo;     // [BH, Cpad, d] bf16 lo part: c - hi
   float* c_norm;      // [BH, Cpad]  ||c||^2 (f32), +inf for padding centroids
   double* c_sum;      // [BH, C, d]  fp64 cluster sums of the update (kept zero between iterations)
+  void* pp;           // k-means++ seeding scratch (kmeanspp_ws_bytes)
 };
+constexpr int kPPMaxBlocks = 64;  // k-means++: CTAs per head
+size_t kmeanspp_ws_bytes(int BH, int N);
 inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   KmeansWs w;
   w.sort = carve_sort(c, BH, N, C);
@@ -65,6 +68,7 @@ inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   w.c_lo = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
   w.c_norm = c.take<float>(size_t(BH) * cent_pad(C));
   w.c_sum = c.take<double>(size_t(BH) * C * d);
+  w.pp = c.take<uint8_t>(kmeanspp_ws_bytes(BH, N));
   return w;
 }
 
@@ -106,9 +110,15 @@ cudaError_t launch_stable_sort(const int32_t* labels, int BH, int N, int C, Sort
 cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const void* X0, void* X0p,
                                const void* X1, void* X1p, cudaStream_t s);
 cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int N, int d, void* O, cudaStream_t s);
+// k-means cold-start options (DESIGN R2, R25): strided rows, or k-means++ with the R25 generator
+struct KmeansInit {
+  bool kmeanspp = false;
+  uint32_t seed = 0;
+  int role = 0;  // 0 = Q, 1 = K (part of the generator's stream id)
+};
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
-                          cudaStream_t s, int* launches);
+                          cudaStream_t s, int* launches, const KmeansInit& init = KmeansInit());
 cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH,
                                int Cq, int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
                                cudaStream_t s);
@@ -118,6 +128,9 @@ cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void
                                       int d, int Cq, int Ck, float scale, const int32_t* q_perm, void* O,
                                       float* lse, AttnWs ws, cudaStream_t s);
 int kmeans_launch_count(int iters, bool warm);
+cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, float* cent,
+                            void* ws, cudaStream_t s);
+int kmeanspp_launch_count(int BH, int N, int d);
 constexpr int kSortLaunches = 3, kWorklistLaunches = 2;
 
 }  // namespace svg2

@@ -86,7 +86,7 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
   if (cfg->iters < 1) return SVG2_ERR_INVALID_PARAM;
   if (!(cfg->top_p > 0.0 && cfg->top_p <= 1.0)) return SVG2_ERR_INVALID_PARAM;
   if (!(cfg->scale >= 0.f) || std::isinf(cfg->scale)) return SVG2_ERR_INVALID_PARAM;
-  if (cfg->flags & ~SVG2_WARM_START) return SVG2_ERR_INVALID_PARAM;
+  if (cfg->flags & ~(SVG2_WARM_START | SVG2_INIT_KMEANSPP)) return SVG2_ERR_INVALID_PARAM;
   return SVG2_OK;
 }
 
@@ -142,23 +142,28 @@ size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dm, const svg2_config
 }
 
 svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C, int32_t iters,
-                          uint32_t flags, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
+                          uint32_t flags, uint32_t seed, int32_t role, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
                           int32_t* offsets, void* ws, size_t ws_bytes, void* stream) {
   if (!X || !centroids || !labels || !sizes || (!ws && ws_bytes)) return SVG2_ERR_NULL_POINTER;
   svg2_status_t st = check_bhnd(B, H, N, d);
   if (st != SVG2_OK) return st;
   if ((st = check_clusters(C, N)) != SVG2_OK) return st;
-  if (iters < 1 || (flags & ~SVG2_WARM_START)) return SVG2_ERR_INVALID_PARAM;
+  if (iters < 1 || (flags & ~(SVG2_WARM_START | SVG2_INIT_KMEANSPP)) || role < 0 || role > 1)
+    return SVG2_ERR_INVALID_PARAM;
   if (!aligned16(X) || !aligned16(centroids)) return SVG2_ERR_MISALIGNED;
-  svg2_config_t cfg{C, C, iters, 1.0, 0.f, flags};
+  svg2_config_t cfg{C, C, iters, 1.0, 0.f, flags, seed};
   svg2_dims_t dm{B, H, N, N, d};
   if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_KMEANS, dm, &cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
   if ((st = check_device()) != SVG2_OK) return st;
   if ((st = pending_error()) != SVG2_OK) return st;
   Carver c(ws);
   KmeansWs kw = carve_kmeans(c, B * H, N, C);
+  KmeansInit init;
+  init.kmeanspp = (flags & SVG2_INIT_KMEANSPP) != 0;
+  init.seed = seed;
+  init.role = role;
   return from_cuda(launch_kmeans(X, B * H, N, d, C, iters, flags & SVG2_WARM_START, centroids, labels, sizes, perm,
-                                 offsets, kw, static_cast<cudaStream_t>(stream), nullptr));
+                                 offsets, kw, static_cast<cudaStream_t>(stream), nullptr, init));
 }
 
 svg2_status_t svg2_permute(const int32_t* labels, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C,
@@ -241,7 +246,10 @@ int32_t svg2_sparse_attention_launch_count(svg2_dims_t dm, const svg2_config_t* 
   (void)dm;
   if (!cfg) return 0;
   const bool warm = cfg->flags & SVG2_WARM_START;
-  return 2 * kmeans_launch_count(cfg->iters, warm) + 2 /*gathers*/ + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+  int n = 2 * kmeans_launch_count(cfg->iters, warm) + 2 /*gathers*/ + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+  if (!warm && (cfg->flags & SVG2_INIT_KMEANSPP))
+    n += kmeanspp_launch_count(dm.B * dm.H, dm.Nq, dm.d) + kmeanspp_launch_count(dm.B * dm.H, dm.Nk, dm.d) - 2;
+  return n;
 }
 
 svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V, svg2_dims_t dm,
@@ -278,12 +286,17 @@ svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V,
   const float scale = resolve_scale(cfg->scale, dm.d);
   cudaError_t e = cudaSuccess;
   mark(0);
+  KmeansInit init_q, init_k;
+  init_q.kmeanspp = init_k.kmeanspp = (cfg->flags & SVG2_INIT_KMEANSPP) != 0;
+  init_q.seed = init_k.seed = cfg->seed;
+  init_q.role = 0;
+  init_k.role = 1;
   e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
-                    w.km, s, nullptr);
+                    w.km, s, nullptr, init_q);
   mark(1);
   if (e == cudaSuccess)
     e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
-                      w.off_k, w.km, s, nullptr);
+                      w.off_k, w.km, s, nullptr, init_k);
   mark(2);
   if (e == cudaSuccess) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
   if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, V, w.Vp, s);

@@ -298,7 +298,8 @@ __global__ void k_init_cold(const __nv_bfloat16* __restrict__ X, int N, int C, f
 }
 
 template <int D>
-cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, float* cent, int32_t* labels,
+cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, const KmeansInit& init,
+                       float* cent, int32_t* labels,
                        int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws, cudaStream_t s) {
   const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(Xv);
   const int Cpad = cent_pad(C);
@@ -312,7 +313,12 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long units = (long long)BH * ((N + kAsgRows - 1) / kAsgRows);
   const int grid_asg = int(units < sms ? units : sms);  // persistent: one CTA per SM
-  if (!warm) k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
+  if (!warm && init.kmeanspp) {
+    cudaError_t e = launch_kmeanspp(Xv, BH, N, D, C, init.seed, init.role, cent, ws.pp, s);
+    if (e != cudaSuccess) return e;
+  } else if (!warm) {
+    k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
+  }
   cudaMemsetAsync(ws.c_sum, 0, size_t(BH) * C * D * sizeof(double), s);
   __nv_bfloat16* hi = reinterpret_cast<__nv_bfloat16*>(ws.c_hi);
   __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
@@ -335,12 +341,16 @@ int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * 
 
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
-                          cudaStream_t s, int* launches) {
+                          cudaStream_t s, int* launches, const KmeansInit& init) {
   if (!perm) perm = ws.perm;
   if (!offsets) offsets = ws.offsets;
-  if (launches) *launches += kmeans_launch_count(iters, warm);
-  if (d == 128) return run_kmeans<128>(X, BH, N, C, iters, warm, centroids, labels, sizes, perm, offsets, ws, s);
-  return run_kmeans<64>(X, BH, N, C, iters, warm, centroids, labels, sizes, perm, offsets, ws, s);
+  if (launches) {
+    *launches += kmeans_launch_count(iters, warm);
+    if (!warm && init.kmeanspp) *launches += kmeanspp_launch_count(BH, N, d) - 1;  // replaces the strided init
+  }
+  if (d == 128)
+    return run_kmeans<128>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s);
+  return run_kmeans<64>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s);
 }
 
 }  // namespace svg2

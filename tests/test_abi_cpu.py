@@ -42,7 +42,7 @@ def test_binding_names_match_abi():
 
 
 def test_status_strings_and_version(lib):
-    assert lib.svg2_abi_version() == 1
+    assert lib.svg2_abi_version() == 2
     assert lib.svg2_status_string(0) == b"SVG2_OK"
     assert lib.svg2_status_string(5) == b"SVG2_ERR_WORKSPACE_TOO_SMALL"
 
@@ -77,6 +77,17 @@ def test_validation_rejects_before_touching_the_device(lib):
     # too-small workspace -> SVG2_ERR_WORKSPACE_TOO_SMALL
     assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg), fake, fake, fake, None, None, fake,
                                      16, None) == 5
+    # unknown flag bits -> SVG2_ERR_INVALID_PARAM; the k-means++ cold-start flag is accepted (then the fake pointers
+    # fail the device check or later, never the parameter check)
+    cfg_flag = m.Config(8, 8, 1, 0.9, 0.0, 4)
+    assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg_flag), fake, fake, fake, None, None,
+                                     fake, 1 << 30, None) == 3
+    cfg_pp = m.Config(8, 8, 1, 0.9, 0.0, m.SVG2_INIT_KMEANSPP, 7)
+    assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg_pp), fake, fake, fake, None, None,
+                                     fake, 1 << 30, None) not in (1, 2, 3, 4, 5)
+    # svg2_kmeans: role must be 0 (queries) or 1 (keys)
+    assert lib.svg2_kmeans(fake, 1, 1, 256, 64, 8, 1, m.SVG2_INIT_KMEANSPP, 7, 2, fake, fake, fake, None, None, fake,
+                           1 << 30, None) == 3
     # d unsupported -> SVG2_ERR_INVALID_SHAPE
     assert lib.svg2_sparse_attention(fake, fake, fake, m.Dims(1, 1, 256, 256, 80), ctypes.byref(cfg), fake, fake,
                                      fake, None, None, fake, 1 << 30, None) == 2

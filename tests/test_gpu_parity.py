@@ -101,6 +101,51 @@ def test_kmeans_dup_ties_and_empty_clusters(svg2, oracle_mod):
     assert np.array_equal(sizes.cpu().numpy()[0, 0], osz)
 
 
+@pytest.mark.parametrize("H,N,d,C,dup", [(3, 3000, 128, 64, False), (2, 1000, 64, 200, False),
+                                         (2, 1024, 64, 40, True)])
+def test_kmeanspp_cold_start_matches_oracle(svg2, oracle_mod, H, N, d, C, dup):
+    """k-means++ seeding with the R25 generator: the GPU picks the oracle's rows, so one Lloyd
+    iteration from them gives the oracle's labels (near-ties aside, R16) and bit-identical centroid means.  With
+    duplicated rows many weights are 0 (and a whole tail of picks can fall on zero-weight fallbacks)."""
+    if dup:
+        wl = svg2_synth.WORKLOADS["tiny"]
+        q, _, _ = svg2_synth.generate(wl, dup=True, heads=range(H))
+    else:
+        q, _, _ = random_qkv(1, H, N, N, d, seed=77 + N, groups=16)
+    X = to_dev(q)
+    B, H, N, d = X.shape
+    seed, role = 12345, 1
+    labels, sizes, cent = svg2.kmeans(X, C, 1, init="kmeans++", seed=seed, role=role)
+    X64 = to_f64(X)
+    for h in range(H):
+        stream = oracle_mod.kmeanspp_stream(0, h, H, role)
+        idx = oracle_mod.kmeanspp_init(X64[0, h], C, seed, stream)
+        init = X64[0, h][idx]
+        gl = labels.cpu().numpy()[0, h]
+        nbad, nontie = label_mismatches_are_ties(X64[0, h], init, gl)
+        assert nontie == 0, f"head {h}: {nontie} labels differ from the oracle's k-means++ seeding"
+        ol, oc, osz = oracle_mod.kmeans(X64[0, h], C, 1, init=init)
+        if nbad == 0:
+            assert np.array_equal(gl, ol)
+            assert np.array_equal(sizes.cpu().numpy()[0, h], osz)
+            assert np.array_equal(cent.cpu().numpy()[0, h], oc.astype(np.float32))
+
+
+def test_fused_call_kmeanspp_cold_start(svg2, oracle_mod):
+    """The fused call's cold start with init="kmeans++" seeds Q with role 0 and K with role 1 (R25) per (b,h)."""
+    wl = svg2_synth.WORKLOADS["tiny"]
+    q, k, v = svg2_synth.generate(wl, heads=range(2))
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    B, H, N, d = Q.shape
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, wl.top_p, debug=True, init="kmeans++", seed=99)
+    for h in range(H):
+        for role, (X, C, key) in enumerate(((Q, wl.Cq, "q"), (K, wl.Ck, "k"))):
+            X64 = to_f64(X)[0, h]
+            ol, oc, osz, idx = oracle_mod.kmeanspp(X64, C, 2, 99, oracle_mod.kmeanspp_stream(0, h, H, role))
+            assert np.array_equal(ex[f"{key}_labels"].cpu().numpy()[0, h], ol), f"head {h} role {key}"
+            assert np.array_equal(ex[f"{key}_centroids"].cpu().numpy()[0, h], oc.astype(np.float32))
+
+
 # ------------------------------------------------------------------ P4: selection
 @pytest.mark.parametrize("p", [0.3, 0.7, 0.9, 0.95, 1.0])
 @pytest.mark.parametrize("Cq,Ck,d", [(16, 32, 64), (100, 500, 128), (37, 1000, 128)])
