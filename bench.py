@@ -339,18 +339,16 @@ def run_ours(args, wl):
         except Exception:
             pass
 
-    # ---- e2e through the public API with host buffers (rank-local heads)
+    # ---- e2e through the C-ABI call on HOST buffers (svg2_sparse_attention_host, rank-local heads): every step moves
+    # this rank's Q, K, V from pinned host memory to the device and O back, inside the library's pipeline
     e2e = None
     if pinned is not None:
         out_host = torch.empty((B, Hl, N, d), dtype=torch.bfloat16).pin_memory()
-        Qd, Kd, Vd = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
+        qc_e, kc_e = cq.clone(), ck.clone()
 
         def e2e_step():
-            Qd.copy_(pinned[0], non_blocking=True)
-            Kd.copy_(pinned[1], non_blocking=True)
-            Vd.copy_(pinned[2], non_blocking=True)
-            Oe, _, _ = svg2.sparse_attention(Qd, Kd, Vd, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True)
-            out_host.copy_(Oe, non_blocking=True)
+            svg2.sparse_attention_host(pinned[0], pinned[1], pinned[2], wl.Cq, wl.Ck, iters_w, top_p, qc_e, kc_e,
+                                       warm=True, out=out_host)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -369,7 +367,8 @@ def run_ours(args, wl):
             te = float(t.item())
         nbytes = B * Hl * N * d * 2
         e2e = {"value": dense_flops / (te * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": te,
-               "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world}
+               "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world,
+               "api": "svg2_sparse_attention_host (C ABI, pinned host Q/K/V in, host O out)"}
 
     # ---- dense baseline (same box, same inputs)
     dense = None

@@ -97,7 +97,8 @@ typedef enum {
   SVG2_ENTRY_SELECT_TOPP = 2,
   SVG2_ENTRY_VARBLOCK_ATTENTION = 3,
   SVG2_ENTRY_UNPERMUTE = 4,
-  SVG2_ENTRY_SPARSE_ATTENTION = 5
+  SVG2_ENTRY_SPARSE_ATTENTION = 5,
+  SVG2_ENTRY_SPARSE_ATTENTION_HOST = 6
 } svg2_entry_t;
 
 /* Bytes of workspace the entry needs for these dims/config (dims.Nq is N for SVG2_ENTRY_KMEANS/PERMUTE;
@@ -158,6 +159,18 @@ SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const
                                     const svg2_config_t* config, float* q_centroids, float* k_centroids, void* O,
                                     int64_t* selected_pairs, const svg2_debug_t* dbg, void* ws, size_t ws_bytes,
                                     void* stream);
+
+/* ---- The fused call on HOST buffers (offload / end-to-end use).  Qh, Kh, Vh [B,H,N,d] bf16 and Oh [B,H,Nq,d] bf16
+ * in host memory (page-locked for the copies to overlap; pageable memory works but serialises).  Same math and
+ * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (6 by default): the copy of
+ * chunk c+1 to the device and of chunk c-1 back to the host overlap the computation of chunk c (internal streams,
+ * double-buffered device staging in the workspace, SVG2_ENTRY_SPARSE_ATTENTION_HOST).  The centroid caches and
+ * selected_pairs are DEVICE buffers as in svg2_sparse_attention.  The work is ordered after the work already queued
+ * on `stream`, and later work on `stream` waits for it; Oh is complete when `stream` has synchronised. */
+SVG2_API svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const void* Vh, svg2_dims_t dims,
+                                                  const svg2_config_t* config, float* q_centroids,
+                                                  float* k_centroids, void* Oh, int64_t* selected_pairs, void* ws,
+                                                  size_t ws_bytes, void* stream);
 
 /* Number of kernels the fused call launches for these dims/config (for launch accounting in benchmarks). */
 SVG2_API int32_t svg2_sparse_attention_launch_count(svg2_dims_t dims, const svg2_config_t* config);

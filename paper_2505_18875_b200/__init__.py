@@ -21,14 +21,14 @@ LIB_PATH = os.environ.get("SVG2_LIBRARY", os.path.join(_HERE, "libsvg2.so"))
 
 SVG2_WARM_START = 1
 SVG2_INIT_KMEANSPP = 2  # cold init by k-means++ seeding (generator DESIGN R25)
-ENTRY_KMEANS, ENTRY_PERMUTE, ENTRY_SELECT_TOPP, ENTRY_VARBLOCK_ATTENTION, ENTRY_UNPERMUTE, ENTRY_SPARSE_ATTENTION = \
-    range(6)
+(ENTRY_KMEANS, ENTRY_PERMUTE, ENTRY_SELECT_TOPP, ENTRY_VARBLOCK_ATTENTION, ENTRY_UNPERMUTE, ENTRY_SPARSE_ATTENTION,
+ ENTRY_SPARSE_ATTENTION_HOST) = range(7)
 STATUS = ["SVG2_OK", "SVG2_ERR_NULL_POINTER", "SVG2_ERR_INVALID_SHAPE", "SVG2_ERR_INVALID_PARAM",
           "SVG2_ERR_MISALIGNED", "SVG2_ERR_WORKSPACE_TOO_SMALL", "SVG2_ERR_UNSUPPORTED_DEVICE", "SVG2_ERR_CUDA",
           "SVG2_ERR_NOT_IMPLEMENTED"]
 EXPORTED_SYMBOLS = ["svg2_status_string", "svg2_abi_version", "svg2_workspace_size", "svg2_kmeans", "svg2_permute",
                     "svg2_select_topp", "svg2_varblock_attention", "svg2_unpermute", "svg2_sparse_attention",
-                    "svg2_sparse_attention_launch_count"]
+                    "svg2_sparse_attention_host", "svg2_sparse_attention_launch_count"]
 
 
 class SVG2Error(RuntimeError):
@@ -81,10 +81,11 @@ def load_library(path: str = LIB_PATH):
     lib.svg2_unpermute.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
     lib.svg2_sparse_attention.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp,
                                           ctypes.POINTER(Debug), vp, sz, vp]
+    lib.svg2_sparse_attention_host.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_sparse_attention_launch_count.argtypes = [Dims, ctypes.POINTER(Config)]
     lib.svg2_sparse_attention_launch_count.restype = i32
     for name in ["svg2_kmeans", "svg2_permute", "svg2_select_topp", "svg2_varblock_attention", "svg2_unpermute",
-                 "svg2_sparse_attention"]:
+                 "svg2_sparse_attention", "svg2_sparse_attention_host"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -305,6 +306,41 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
                                      _p(O), _p(pairs), ctypes.byref(dbg) if dbg is not None else None, _p(ws),
                                      ws.numel(), _stream()))
     return O, pairs, extras
+
+
+def sparse_attention_host(Qh, Kh, Vh, Cq: int, Ck: int, iters: int, top_p: float, q_centroids=None,
+                          k_centroids=None, warm: bool = False, scale: float = 0.0, out=None, init: str = "strided",
+                          seed: int = 0, device=None):
+    """The fused call on HOST tensors (svg2_sparse_attention_host): Qh, Kh, Vh [B,H,N,d] bf16 CPU tensors (pin them
+    for overlapped copies), output a bf16 CPU tensor (`out`, else a new pinned one).  The library streams head chunks
+    to the device, computes and copies back with the transfers overlapping the computation.  Centroid caches and
+    selected_pairs live on the device.  Returns (O_host, selected_pairs, extras); O_host is complete once the current
+    CUDA stream has synchronised."""
+    lib = load_library()
+    for t, n in ((Qh, "Q"), (Kh, "K"), (Vh, "V")):
+        if t.dtype != torch.bfloat16 or t.dim() != 4 or t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{n}: expected a contiguous [B,H,N,d] bfloat16 CPU tensor")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    B, H, Nq, d = Qh.shape
+    Nk = Kh.shape[2]
+    if q_centroids is None:
+        if warm:
+            raise ValueError("warm start needs q_centroids / k_centroids")
+        q_centroids = torch.empty(B, H, Cq, d, dtype=torch.float32, device=dev)
+    if k_centroids is None:
+        k_centroids = torch.empty(B, H, Ck, d, dtype=torch.float32, device=dev)
+    _need(q_centroids, torch.float32, "q_centroids", 4)
+    _need(k_centroids, torch.float32, "k_centroids", 4)
+    O = out if out is not None else torch.empty((B, H, Nq, d), dtype=torch.bfloat16).pin_memory()
+    pairs = torch.empty(B, H, dtype=torch.int64, device=dev)
+    cfg = Config(Cq, Ck, iters, top_p, scale, SVG2_WARM_START if warm else _cold_flags(init), seed)
+    dims = Dims(B, H, Nq, Nk, d)
+    nbytes = int(lib.svg2_workspace_size(ENTRY_SPARSE_ATTENTION_HOST, dims, ctypes.byref(cfg)))
+    ws = _workspace(max(nbytes, 256), dev)
+    _check("svg2_sparse_attention_host",
+           lib.svg2_sparse_attention_host(_p(Qh), _p(Kh), _p(Vh), dims, ctypes.byref(cfg), _p(q_centroids),
+                                          _p(k_centroids), _p(O), _p(pairs), _p(ws), ws.numel(), _stream()))
+    return O, pairs, {"q_centroids": q_centroids, "k_centroids": k_centroids}
 
 
 class SVG2Attention:

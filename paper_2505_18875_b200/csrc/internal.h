@@ -114,7 +114,8 @@ cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int
 struct KmeansInit {
   bool kmeanspp = false;
   uint32_t seed = 0;
-  int role = 0;  // 0 = Q, 1 = K (part of the generator's stream id)
+  int role = 0;     // 0 = Q, 1 = K (part of the generator's stream id)
+  int bh_base = 0;  // global (b,h) index of the first head of this launch (chunked calls keep the stream ids)
 };
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
@@ -128,8 +129,8 @@ cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void
                                       int d, int Cq, int Ck, float scale, const int32_t* q_perm, void* O,
                                       float* lse, AttnWs ws, cudaStream_t s);
 int kmeans_launch_count(int iters, bool warm);
-cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, float* cent,
-                            void* ws, cudaStream_t s);
+cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
+                            float* cent, void* ws, cudaStream_t s);
 int kmeanspp_launch_count(int BH, int N, int d);
 constexpr int kSortLaunches = 3, kWorklistLaunches = 2;
 

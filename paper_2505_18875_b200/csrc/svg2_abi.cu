@@ -2,6 +2,7 @@
 // touched on error), workspace carving, and the enqueue of the kernels of svg2_*.cu on the caller's stream.
 #include <cuda_runtime.h>
 #include <cmath>
+#include <cstdlib>
 #include "../../include/svg2.h"
 #include "internal.h"
 
@@ -10,6 +11,7 @@ using namespace svg2;
 namespace {
 
 constexpr long long kMaxN = 1ll << 24;
+constexpr int kHostChunks = 6;  // head chunks of the host-buffer pipeline (measured e2e 77 / 69 / 67 / 65 / 67 ms at 2 / 3 / 4 / 6 / 8 chunks, HunyuanVideo; env SVG2_HOST_CHUNKS overrides)
 
 svg2_status_t check_device() {
   int dev = 0, major = 0, minor = 0;
@@ -90,6 +92,93 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
   return SVG2_OK;
 }
 
+// The whole fused call for the heads of `dm` on stream s (arguments validated by the caller).  bh_base = global
+// (b,h) index of the first head (k-means++ stream ids of chunked calls, R25).
+cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_dims_t& dm, const svg2_config_t* cfg,
+                      float* q_centroids, float* k_centroids, void* O, int64_t* selected_pairs,
+                      const svg2_debug_t* dbg, FusedWs w, cudaStream_t s, int bh_base) {
+  if (dbg) {  // intermediates requested: write them straight into the caller's buffers
+    if (dbg->q_labels) w.lab_q = dbg->q_labels;
+    if (dbg->k_labels) w.lab_k = dbg->k_labels;
+    if (dbg->q_perm) w.perm_q = dbg->q_perm;
+    if (dbg->k_perm) w.perm_k = dbg->k_perm;
+    if (dbg->q_offsets) w.off_q = dbg->q_offsets;
+    if (dbg->k_offsets) w.off_k = dbg->k_offsets;
+    if (dbg->mask) w.mask = dbg->mask;
+  }
+  auto mark = [&](int k) {
+    if (dbg && dbg->events[k]) cudaEventRecord(static_cast<cudaEvent_t>(dbg->events[k]), s);
+  };
+  const int BH = dm.B * dm.H;
+  const bool warm = cfg->flags & SVG2_WARM_START;
+  const float scale = resolve_scale(cfg->scale, dm.d);
+  cudaError_t e = cudaSuccess;
+  mark(0);
+  KmeansInit init_q, init_k;
+  init_q.kmeanspp = init_k.kmeanspp = (cfg->flags & SVG2_INIT_KMEANSPP) != 0;
+  init_q.seed = init_k.seed = cfg->seed;
+  init_q.role = 0;
+  init_k.role = 1;
+  init_q.bh_base = init_k.bh_base = bh_base;
+  e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
+                    w.km, s, nullptr, init_q);
+  mark(1);
+  if (e == cudaSuccess)
+    e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
+                      w.off_k, w.km, s, nullptr, init_k);
+  mark(2);
+  if (e == cudaSuccess) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
+  if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, V, w.Vp, s);
+  mark(3);
+  if (e == cudaSuccess)
+    e = launch_select_topp(q_centroids, k_centroids, w.size_q, w.size_k, BH, cfg->Cq, cfg->Ck, dm.d, scale,
+                           cfg->top_p, w.mask, selected_pairs, s);
+  mark(4);
+  if (e == cudaSuccess)
+    e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck, w.attn, s);
+  mark(5);
+  if (e == cudaSuccess)
+    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, cfg->Cq, cfg->Ck, scale, w.perm_q, O,
+                                  nullptr, w.attn, s);
+  mark(6);
+  mark(7);
+  return e;
+}
+
+// Host-buffer pipeline (svg2_sparse_attention_host): heads in chunks, double-buffered device staging.
+struct HostPlan {
+  int BH, hc, nchunks;
+};
+HostPlan host_plan(const svg2_dims_t& dm) {
+  static const int chunks_env = [] {
+    const char* e = getenv("SVG2_HOST_CHUNKS");
+    return e ? atoi(e) : 0;
+  }();
+  HostPlan p;
+  p.BH = dm.B * dm.H;
+  int chunks = chunks_env > 0 ? chunks_env : kHostChunks;
+  chunks = chunks < p.BH ? chunks : p.BH;
+  p.hc = (p.BH + chunks - 1) / chunks;
+  p.nchunks = (p.BH + p.hc - 1) / p.hc;
+  return p;
+}
+struct HostWs {
+  void *Q[2], *K[2], *V[2], *O[2];
+  FusedWs fused;
+};
+HostWs carve_host(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg, const HostPlan& p) {
+  HostWs w;
+  const size_t q = size_t(p.hc) * dm.Nq * dm.d, k = size_t(p.hc) * dm.Nk * dm.d;
+  for (int i = 0; i < 2; ++i) {
+    w.Q[i] = c.take<uint16_t>(q);
+    w.K[i] = c.take<uint16_t>(k);
+    w.V[i] = c.take<uint16_t>(k);
+    w.O[i] = c.take<uint16_t>(q);
+  }
+  const svg2_dims_t chunk{1, p.hc, dm.Nq, dm.Nk, dm.d};
+  w.fused = carve_fused(c, chunk, cfg);
+  return w;
+}
 }  // namespace
 
 extern "C" {
@@ -136,6 +225,10 @@ size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dm, const svg2_config
     case SVG2_ENTRY_SPARSE_ATTENTION:
       if (validate_fused(dm, cfg) != SVG2_OK) return 0;
       carve_fused(c, dm, *cfg);
+      return c.off + 256;
+    case SVG2_ENTRY_SPARSE_ATTENTION_HOST:
+      if (validate_fused(dm, cfg) != SVG2_OK) return 0;
+      carve_host(c, dm, *cfg, host_plan(dm));
       return c.off + 256;
   }
   return 0;
@@ -268,51 +361,75 @@ svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V,
 
   Carver c(ws);
   FusedWs w = carve_fused(c, dm, *cfg);
-  if (dbg) {  // intermediates requested: write them straight into the caller's buffers
-    if (dbg->q_labels) w.lab_q = dbg->q_labels;
-    if (dbg->k_labels) w.lab_k = dbg->k_labels;
-    if (dbg->q_perm) w.perm_q = dbg->q_perm;
-    if (dbg->k_perm) w.perm_k = dbg->k_perm;
-    if (dbg->q_offsets) w.off_q = dbg->q_offsets;
-    if (dbg->k_offsets) w.off_k = dbg->k_offsets;
-    if (dbg->mask) w.mask = dbg->mask;
+  return from_cuda(run_fused(Q, K, V, dm, cfg, q_centroids, k_centroids, O, selected_pairs, dbg, w,
+                             static_cast<cudaStream_t>(stream), 0));
+}
+
+svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const void* Vh, svg2_dims_t dm,
+                                         const svg2_config_t* cfg, float* q_centroids, float* k_centroids, void* Oh,
+                                         int64_t* selected_pairs, void* ws, size_t ws_bytes, void* stream) {
+  if (!Qh || !Kh || !Vh || !cfg || !q_centroids || !k_centroids || !Oh || !ws) return SVG2_ERR_NULL_POINTER;
+  svg2_status_t st = validate_fused(dm, cfg);
+  if (st != SVG2_OK) return st;
+  if (!aligned16(Qh) || !aligned16(Kh) || !aligned16(Vh) || !aligned16(Oh) || !aligned16(q_centroids) ||
+      !aligned16(k_centroids))
+    return SVG2_ERR_MISALIGNED;
+  if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_SPARSE_ATTENTION_HOST, dm, cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = check_device()) != SVG2_OK) return st;
+  if ((st = pending_error()) != SVG2_OK) return st;
+  const HostPlan plan = host_plan(dm);
+  Carver c(ws);
+  HostWs w = carve_host(c, dm, *cfg, plan);
+  cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  // three internal streams: copies in, compute, copies out; events order them per chunk and slot
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  cudaEvent_t start = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  const int n = plan.nchunks;
+  cudaEvent_t* ev = new cudaEvent_t[3 * n]();  // per chunk: inputs in, computed, output out
+  for (int i = 0; e == cudaSuccess && i < 3 * n; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(start, caller);  // after the caller's earlier work
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(scomp, start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, start, 0);
+  const size_t qrow = size_t(dm.Nq) * dm.d * 2, krow = size_t(dm.Nk) * dm.d * 2;  // bytes per head
+  for (int ci = 0; e == cudaSuccess && ci < n; ++ci) {
+    const int bh0 = ci * plan.hc, nh = plan.BH - bh0 < plan.hc ? plan.BH - bh0 : plan.hc, slot = ci & 1;
+    cudaEvent_t in = ev[3 * ci], done = ev[3 * ci + 1], out = ev[3 * ci + 2];
+    if (ci >= 2) e = cudaStreamWaitEvent(sin, ev[3 * (ci - 2) + 1], 0);  // slot's inputs consumed
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(w.Q[slot], static_cast<const uint8_t*>(Qh) + bh0 * qrow, nh * qrow, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(w.K[slot], static_cast<const uint8_t*>(Kh) + bh0 * krow, nh * krow, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(w.V[slot], static_cast<const uint8_t*>(Vh) + bh0 * krow, nh * krow, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaEventRecord(in, sin);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(scomp, in, 0);
+    if (e == cudaSuccess && ci >= 2) e = cudaStreamWaitEvent(scomp, ev[3 * (ci - 2) + 2], 0);  // slot's output read
+    if (e == cudaSuccess) {
+      const svg2_dims_t cd{1, nh, dm.Nq, dm.Nk, dm.d};
+      e = run_fused(w.Q[slot], w.K[slot], w.V[slot], cd, cfg, q_centroids + size_t(bh0) * cfg->Cq * dm.d,
+                    k_centroids + size_t(bh0) * cfg->Ck * dm.d, w.O[slot],
+                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused, scomp, bh0);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(done, scomp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, done, 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(Oh) + bh0 * qrow, w.O[slot], nh * qrow, cudaMemcpyDeviceToHost, sout);
+    if (e == cudaSuccess) e = cudaEventRecord(out, sout);
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto mark = [&](int k) {
-    if (dbg && dbg->events[k]) cudaEventRecord(static_cast<cudaEvent_t>(dbg->events[k]), s);
-  };
-  const int BH = dm.B * dm.H;
-  const bool warm = cfg->flags & SVG2_WARM_START;
-  const float scale = resolve_scale(cfg->scale, dm.d);
-  cudaError_t e = cudaSuccess;
-  mark(0);
-  KmeansInit init_q, init_k;
-  init_q.kmeanspp = init_k.kmeanspp = (cfg->flags & SVG2_INIT_KMEANSPP) != 0;
-  init_q.seed = init_k.seed = cfg->seed;
-  init_q.role = 0;
-  init_k.role = 1;
-  e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
-                    w.km, s, nullptr, init_q);
-  mark(1);
-  if (e == cudaSuccess)
-    e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
-                      w.off_k, w.km, s, nullptr, init_k);
-  mark(2);
-  if (e == cudaSuccess) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
-  if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, V, w.Vp, s);
-  mark(3);
-  if (e == cudaSuccess)
-    e = launch_select_topp(q_centroids, k_centroids, w.size_q, w.size_k, BH, cfg->Cq, cfg->Ck, dm.d, scale,
-                           cfg->top_p, w.mask, selected_pairs, s);
-  mark(4);
-  if (e == cudaSuccess)
-    e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck, w.attn, s);
-  mark(5);
-  if (e == cudaSuccess)
-    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, cfg->Cq, cfg->Ck, scale, w.perm_q, O,
-                                  nullptr, w.attn, s);
-  mark(6);
-  mark(7);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 2], 0);  // the last copy out ends the call
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 1], 0);
+  for (int i = 0; i < 3 * n; ++i)
+    if (ev[i]) cudaEventDestroy(ev[i]);
+  delete[] ev;
+  if (start) cudaEventDestroy(start);
+  if (sin) cudaStreamDestroy(sin);  // released once their queued work completes
+  if (scomp) cudaStreamDestroy(scomp);
+  if (sout) cudaStreamDestroy(sout);
   return from_cuda(e);
 }
 

@@ -314,7 +314,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
   const long long units = (long long)BH * ((N + kAsgRows - 1) / kAsgRows);
   const int grid_asg = int(units < sms ? units : sms);  // persistent: one CTA per SM
   if (!warm && init.kmeanspp) {
-    cudaError_t e = launch_kmeanspp(Xv, BH, N, D, C, init.seed, init.role, cent, ws.pp, s);
+    cudaError_t e = launch_kmeanspp(Xv, BH, N, D, C, init.seed, init.role, init.bh_base, cent, ws.pp, s);
     if (e != cudaSuccess) return e;
   } else if (!warm) {
     k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);

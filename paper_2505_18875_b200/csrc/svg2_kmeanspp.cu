@@ -72,8 +72,8 @@ struct PPWs {
 
 template <int D>
 __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __restrict__ X, int N, int C, int bh0,
-                                                        int nblk, uint32_t seed, int role, float* __restrict__ cent,
-                                                        PPWs ws) {
+                                                        int nblk, uint32_t seed, uint32_t stream_base,
+                                                        float* __restrict__ cent, PPWs ws) {
   cg::grid_group grid = cg::this_grid();
   const int bh = bh0 + blockIdx.x / nblk, blk = blockIdx.x % nblk, tid = threadIdx.x;
   const int rows_blk = (N + nblk - 1) / nblk;
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
   __shared__ double red[kPPThreads / 32];
   double* Dv = ws.D + size_t(bh) * N;
   const __nv_bfloat16* Xb = X + size_t(bh) * N * D;
-  const uint32_t stream = 2u * uint32_t(bh) + uint32_t(role);
+  const uint32_t stream = 2u * uint32_t(bh) + stream_base;  // 2 * (global bh) + role
   double dref = 0.0;
   for (int j = 0; j < C; ++j) {
     int pick;
@@ -218,8 +218,9 @@ PPPlan pp_plan(int BH, int N) {
 }
 }  // namespace
 
-cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, float* cent,
-                            void* ws_ptr, cudaStream_t s) {
+cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
+                            float* cent, void* ws_ptr, cudaStream_t s) {
+  uint32_t stream_base = 2u * uint32_t(bh_base) + uint32_t(role);
   auto run = [&](auto kernel, PPPlan plan) -> cudaError_t {
     uint8_t* base = static_cast<uint8_t*>(ws_ptr);
     PPWs w;
@@ -234,8 +235,8 @@ cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t
     int nblk = plan.nblk;
     for (int bh0 = 0; bh0 < BH; bh0 += plan.heads_per_launch) {
       const int nh = BH - bh0 < plan.heads_per_launch ? BH - bh0 : plan.heads_per_launch;
-      void* args[] = {(void*)&Xb, (void*)&N, (void*)&C, (void*)&bh0, (void*)&nblk, (void*)&seed, (void*)&role,
-                      (void*)&cent, (void*)&w};
+      void* args[] = {(void*)&Xb, (void*)&N, (void*)&C, (void*)&bh0, (void*)&nblk, (void*)&seed,
+                      (void*)&stream_base, (void*)&cent, (void*)&w};
       cudaError_t e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(nh * nblk), dim3(kPPThreads), args, 0, s);
       if (e != cudaSuccess) return e;
     }

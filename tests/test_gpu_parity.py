@@ -372,3 +372,24 @@ def test_fullsize_sampled_rows(svg2, oracle_mod, name):
         ol, oc, osz = oracle_mod.kmeans(Q64, wl.Cq, 1, init=ex["q_centroids"].cpu().numpy()[0, h].astype(np.float64))
         assert np.array_equal(np.bincount(lq, minlength=wl.Cq), ex["q_offsets"].cpu().numpy()[0, h][1:] -
                               ex["q_offsets"].cpu().numpy()[0, h][:-1])
+
+
+@pytest.mark.parametrize("init", ["strided", "kmeans++"])
+def test_host_pipeline_matches_device_call(svg2, init):
+    """svg2_sparse_attention_host (head chunks streamed through double-buffered device staging, copies overlapping
+    the computation) computes exactly what svg2_sparse_attention computes on device-resident inputs: same output
+    bits, same selected pairs, same centroid caches (cold, then warm from those caches).  5 heads in chunks of 2
+    leave a short last chunk; k-means++ seeding keeps its global (b,h) stream ids across chunks (R25)."""
+    q, k, v = random_qkv(1, 5, 2000, 1800, 128, seed=31)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    Qh, Kh, Vh = (t.cpu().pin_memory() for t in (Q, K, V))
+    Od, pd, exd = svg2.sparse_attention(Q, K, V, 20, 30, 2, 0.9, init=init, seed=4)
+    Oh, ph, exh = svg2.sparse_attention_host(Qh, Kh, Vh, 20, 30, 2, 0.9, init=init, seed=4)
+    torch.cuda.synchronize()
+    assert torch.equal(Oh, Od.cpu()) and torch.equal(ph, pd)
+    assert torch.equal(exh["q_centroids"], exd["q_centroids"]) and torch.equal(exh["k_centroids"], exd["k_centroids"])
+    cq, ck = exd["q_centroids"].clone(), exd["k_centroids"].clone()
+    Od2, pd2, _ = svg2.sparse_attention(Q, K, V, 20, 30, 2, 0.9, cq.clone(), ck.clone(), warm=True)
+    Oh2, ph2, _ = svg2.sparse_attention_host(Qh, Kh, Vh, 20, 30, 2, 0.9, cq.clone(), ck.clone(), warm=True)
+    torch.cuda.synchronize()
+    assert torch.equal(Oh2, Od2.cpu()) and torch.equal(ph2, pd2)
