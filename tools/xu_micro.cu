@@ -23,6 +23,12 @@ __device__ __forceinline__ uint32_t pack_alu(float a, float b) {  // round-half-
   return __byte_perm(ua, ub, 0x7632);
 }
 
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 template <int kMode>
 __global__ void k_bench(float* out, long long* cyc, float seed) {
   float v[kChains];
@@ -39,7 +45,12 @@ __global__ void k_bench(float* out, long long* cyc, float seed) {
       if (kMode == 2) { v[c] = ex2(v[c]); if (c & 1) acc ^= pack(v[c - 1], v[c]); }  // softmax ratio 2 ex2 : 1 pack
       if (kMode == 3) { v[c] = ex2(v[c]); if (c & 1) acc ^= pack_alu(v[c - 1], v[c]); }  // same with ALU pack
       if (kMode == 4) { v[c] = ex2(v[c]); if (c & 1) acc ^= __float_as_uint(v[c - 1] + v[c]); }  // no pack (FADD)
-      if (kMode >= 5) {  // independent inputs: the real softmax shape (x = s*c - m; p = ex2(x); sum; pack)
+      if (kMode == 8) {  // packed bf16x2 exp2: two results per MUFU op?
+        uint32_t u = __float_as_uint(v[c]);
+        u = ex2_bf16x2(u & 0xBFFFBFFFu);
+        v[c] = __uint_as_float(u & 0x3F7F3F7Fu);
+      }
+      if (kMode >= 5 && kMode <= 7) {  // independent inputs: the real softmax shape (x = s*c - m; p = ex2(x); sum; pack)
         const float x0 = fmaf(v[c], 1.4427f, -float(i & 7)), x1 = fmaf(v[(c + 1) % kChains], 1.4427f, -float(i & 3));
         const float p0 = ex2(x0), p1 = ex2(x1);
         v[c] += 1e-9f * (p0 + p1);
@@ -88,5 +99,6 @@ int main() {
   run<5>("indep: ffma ex2 fadd", 2 * kChains, 0);
   run<6>("indep: + F2FP", 2 * kChains, kChains);
   run<7>("indep: + ALU pack", 2 * kChains, kChains);
+  run<8>("ex2.bf16x2 (2 per op)", 2 * kChains, 0);
   return 0;
 }
