@@ -487,7 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mt = fmaxf(mx0, mx1) * sl2;
         if (t == t_first) {
           m_used = mt;
-        } else if (__any_sync(0xffffffffu, mt > m_used + p.rescale_thr)) {
+        } else if (__any_sync(0xffffffffu, rloc < nrows && mt > m_used + p.rescale_thr)) {
+          // only rows of the cluster vote: the tile's padding rows hold whatever follows the cluster in Q'
+          // (another cluster or head), and must not change how the cluster's rows are rounded
           // warp-uniform branch (tcgen05.ld/st are .sync.aligned); rows whose max did not grow get alpha = 1
           const float m_new = fmaxf(m_used, mt);
           const float alpha = ex2_approx(m_used - m_new);

@@ -426,7 +426,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mt = fmaxf(mx0, mx1) * sl2;
         if (n == 0) {
           m_used = mt;
-        } else if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+        } else if (__any_sync(0xffffffffu, rloc < nrows && mt > m_used + kRescaleThreshold)) {
+          // only rows of the cluster vote: the tile's padding rows hold whatever follows the cluster in Q'
+          // (another cluster or head), and must not change how the cluster's rows are rounded
           // warp-uniform branch (tcgen05.ld/st are .sync.aligned); rows whose max did not grow get alpha = 1.
           // O may only be touched once the previous PV of this tile has completed (PV(n) waits for our P(n)).
           mbar_wait(&bars.pv_done[g], (pv_count - 1) & 1, 19);

@@ -412,7 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool pv_done = false;  // PV_g(t-1) known complete (p_free consumed for this tile)
         if (t == 0) {
           m_used = mt;
-        } else if (__any_sync(0xffffffffu, mt > m_used + p.rescale_thr)) {
+        } else if (__any_sync(0xffffffffu, rloc < nrows && mt > m_used + p.rescale_thr)) {
+          // only rows of the cluster vote: the tile's padding rows hold whatever follows the cluster in Q'
+          // (another cluster or head), and must not change how the cluster's rows are rounded
           // O_g must hold all of PV_g(t-1) before it is rescaled
           mbar_wait(&bars.p_free[g], pfph ^ 1, 20 + g);
           pfph ^= 1;

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
   __shared__ double c_s[D];
   __shared__ unsigned long long incl[kPPThreads];  // inclusive scan of the per-thread weight sums
   __shared__ double red[kPPThreads / 32];
+  __shared__ unsigned long long part_s[kPPMaxBlocks];
   double* Dv = ws.D + size_t(bh) * N;
   const __nv_bfloat16* Xb = X + size_t(bh) * N * D;
   const uint32_t stream = 2u * uint32_t(bh) + stream_base;  // 2 * (global bh) + role
@@ -130,10 +131,20 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
         ws.bmax[size_t(bh) * nblk + blk] = m;
       }
       grid.sync();
-      for (int b = 0; b < nblk; ++b) {
-        const double m = *((volatile double*)(ws.bmax + size_t(bh) * nblk + b));
-        dref = m > dref ? m : dref;
+      if (tid < 32) {  // the head's CTA maxima: loaded in parallel, reduced in one warp
+        double m = 0.0;
+        for (int b = tid; b < nblk; b += 32) {
+          const double v = *((volatile double*)(ws.bmax + size_t(bh) * nblk + b));
+          m = v > m ? v : m;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double y = __shfl_xor_sync(0xffffffffu, m, o);
+          m = y > m ? y : m;
+        }
+        if (tid == 0) red[0] = m;
       }
+      __syncthreads();
+      dref = red[0];
       for (int n = t0; n < t1; ++n) wsum += pp_weight(Dv[n], dref);
     }
     // block inclusive scan of the per-thread sums (kept in smem for the search below)
@@ -150,17 +161,20 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
     // pick j+1: total over the head's CTAs, sampled position r, owning CTA, owning thread, row
     uint32_t c4[4] = {uint32_t(j + 1), 0u, 0u, 0u};
     philox4x32_10(c4, seed, stream);
+    // the head's per-CTA sums, loaded in parallel into shared memory (one load latency, not nblk)
+    if (tid < nblk) part_s[tid] = *((volatile unsigned long long*)(ws.part + size_t(bh) * nblk + tid));
+    __syncthreads();
     unsigned long long total = 0, before = 0;
     int owner = -1;
     const unsigned long long r64 = uint64_t(c4[0]) | (uint64_t(c4[1]) << 32);
-    for (int b = 0; b < nblk; ++b) total += *((volatile unsigned long long*)(ws.part + size_t(bh) * nblk + b));
+    for (int b = 0; b < nblk; ++b) total += part_s[b];
     if (total == 0) {
       if (blk == 0 && tid == 0) ws.pick[bh] = int((uint64_t(c4[0]) * uint64_t(N)) >> 32);
     } else {
       const unsigned long long r = __umul64hi(r64, total);
       unsigned long long acc = 0;
       for (int b = 0; b < nblk && owner < 0; ++b) {
-        const unsigned long long pb = *((volatile unsigned long long*)(ws.part + size_t(bh) * nblk + b));
+        const unsigned long long pb = part_s[b];
         if (r < acc + pb) {
           owner = b;
           before = acc;

@@ -393,3 +393,38 @@ def test_host_pipeline_matches_device_call(svg2, init):
     Oh2, ph2, _ = svg2.sparse_attention_host(Qh, Kh, Vh, 20, 30, 2, 0.9, cq.clone(), ck.clone(), warm=True)
     torch.cuda.synchronize()
     assert torch.equal(Oh2, Od2.cpu()) and torch.equal(ph2, pd2)
+
+
+def test_maximum_cluster_counts(svg2, oracle_mod):
+    """C = 4096 (the largest supported count): 32 centroid chunks in the assign kernel, the 4096-wide bitonic sort of
+    the selection, and a worklist with thousands of tiny key clusters, all against the oracle."""
+    q, k, v = random_qkv(1, 1, 8192, 8192, 64, seed=41, groups=64)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    X64 = to_f64(K)[0, 0]
+    C = 4096
+    cent = torch.from_numpy(X64[(np.arange(C) * 8192) // C].astype(np.float32)).cuda().view(1, 1, C, 64).contiguous()
+    c64 = cent.cpu().numpy().astype(np.float64)[0, 0]
+    labels, sizes, cent2 = svg2.kmeans(K, C, 1, centroids=cent.clone())
+    nbad, nontie = label_mismatches_are_ties(X64, c64, labels.cpu().numpy()[0, 0])
+    assert nontie == 0
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, 64, C, 1, 0.9, debug=True)
+    lq, lk, m = ex["q_labels"].cpu().numpy()[0, 0], ex["k_labels"].cpu().numpy()[0, 0], ex["mask"].cpu().numpy()[0, 0]
+    rows = np.arange(0, 8192, 37)
+    ref = oracle_mod.attention_rows(to_f64(Q)[0, 0], to_f64(K)[0, 0], to_f64(V)[0, 0], f32scale(64), rows=rows,
+                                    lq=lq, lk=lk, mask=m)
+    check_attention(O[0, 0][torch.from_numpy(rows).cuda()], ref, "C = 4096")
+
+
+def test_heads_are_independent_bitwise(svg2):
+    """Every step is per (b,h): running 4 heads in one call or each head alone (what head-parallel
+    sharding over GPUs does) gives bit-identical outputs and selections.  Guards against cross-head coupling such as
+    padding rows of a partial Q tile (which hold the next head's rows) taking part in warp-uniform decisions."""
+    q, k, v = random_qkv(1, 4, 1500, 1500, 128, seed=53)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, 13, 21, 3, 0.9)
+    for h in range(4):
+        Qh, Kh, Vh = (t[:, h:h + 1].contiguous() for t in (Q, K, V))
+        Oh, ph, exh = svg2.sparse_attention(Qh, Kh, Vh, 13, 21, 3, 0.9)
+        assert torch.equal(Oh[0, 0], O[0, h]), f"head {h}"
+        assert torch.equal(ph[0, 0], pairs[0, h])
+        assert torch.equal(exh["q_centroids"][0, 0], ex["q_centroids"][0, h])
