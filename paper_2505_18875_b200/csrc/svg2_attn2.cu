@@ -49,7 +49,7 @@ constexpr int kRegsCtl = 88, kRegsSoftmax = 208, kRegsLaunch = 168;
 static_assert(128 * kRegsCtl + 256 * kRegsSoftmax <= kRegsLaunch * kThreads, "setmaxnreg budget exceeds launch");
 constexpr int kWarpProducer = 8, kWarpTmem = 9, kWarpMma = 11;  // warp 10 idle
 constexpr int kItemConsumers = 1 + 8;  // the MMA warp + 8 softmax warps arrive on item_empty
-constexpr int kDefaultPoly = 6;  // measured: 48.3-48.5 ms vs 48.8-49.0 ms with 0 (HunyuanVideo, r01)
+constexpr int kDefaultPoly = 4;  // measured (interleaved, HunyuanVideo): 49.0 / 49.9 / 51.2 / 54.4 ms at 4 / 6 / 8 / 10
 
 template <int D>
 struct Cfg {
@@ -138,7 +138,7 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
 
 // kPoly: in every 16-pair chunk of a row's 128 exponentials, kPoly pairs take 2^x on the FMA/ALU pipes (ex2_poly2)
 // instead of MUFU, which otherwise bounds the softmax (16 ex2/clk/SM; tools/xu_micro.cu).  Env SVG2_EXP_POLY
-// (0, 2, 4, 6) selects the split for measurements.
+// (0, 2, 4, 6, 8, 10) selects the split for measurements.
 template <int D, int kPoly>
 __global__ void __launch_bounds__(kThreads, 1)
     k_varblock_attn(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ KVMaps kv, const Params p) {
@@ -687,6 +687,8 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
   if (poly == 2) launch(k_varblock_attn<D, 2>);
   else if (poly == 4) launch(k_varblock_attn<D, 4>);
   else if (poly == 6) launch(k_varblock_attn<D, 6>);
+  else if (poly == 8) launch(k_varblock_attn<D, 8>);
+  else if (poly == 10) launch(k_varblock_attn<D, 10>);
   else launch(k_varblock_attn<D, 0>);
   return cudaGetLastError();
 }
