@@ -90,22 +90,24 @@ struct Params {
   int debug_mode;  // measurement only (env SVG2_DEBUG_MODE): 1 = softmax skips max/exp (P = 0), 2 = cycle trace
 };
 
-// Cycle trace of the first item of CTA 0 (SVG2_DEBUG_MODE=2 with the SVG2_TRACE_PRINT build, measurement only):
-// clock64 per tile and event, printed at kernel exit.  Events: 0/2 MMA a/b saw P, 1/3 MMA a/b finished issuing
-// PV+S, 4/6 softmax a/b got S, 5/7 softmax a/b handed P over, 8/9 producer issued K/V.
-constexpr int kTraceTiles = 48, kTraceEvents = 10;
+// Cycle trace of the first item of CTA 0 (SVG2_DEBUG_MODE=2 with the SVG2_TRACE_PRINT build only; the product
+// build compiles no trace code): clock64 per tile and event, printed at kernel exit.  Events: 0/2 MMA a/b saw P,
+// 1/3 MMA a/b finished issuing PV+S, 4/6 softmax a/b got S, 5/7 softmax a/b handed P over, 8/9 producer issued K/V,
+// 10/11 softmax a/b has S in registers, 12/13 softmax a/b has the max (and any rescale), 14/15 softmax a/b issued
+// all P stores.
+constexpr int kTraceTiles = 48, kTraceEvents = 16;
+#ifdef SVG2_TRACE_PRINT
 #define TRACE(ev, t)                                                                                      \
   do {                                                                                                    \
     if (p.debug_mode == 2 && blockIdx.x == 0 && n_done == 0 && (t) < kTraceTiles && (threadIdx.x & 31) == 0) \
       trace_buf[(ev)*kTraceTiles + (t)] = clock64();                                                      \
   } while (0)
-#ifdef SVG2_TRACE_PRINT
-#define TRACE_MMA(ev, t) TRACE(ev, t)
 #else
-#define TRACE_MMA(ev, t) \
-  do {                   \
+#define TRACE(ev, t) \
+  do {               \
   } while (0)
 #endif
+#define TRACE_MMA(ev, t) TRACE(ev, t)
 
 // Loads one 16-group tile of the item's key stream into a K or V stage.  Lanes 0..ngt-1 hold one group each; a
 // lane whose group does not continue the previous lane's full group starts a run segment and issues power-of-two
@@ -152,8 +154,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_slot;
   __shared__ int4 item_slot[2];
   __shared__ float2 merge_ml[kQTile];  // split items: (m, l) of warpgroup b's rows
+#ifdef SVG2_TRACE_PRINT
   __shared__ long long trace_buf[kTraceEvents * kTraceTiles];
   __shared__ int trace_T;
+#endif
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   int n_done = 0;  // items finished by this role (the trace covers the first one)
@@ -241,7 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             kph ^= 1;
           }
         }
+#ifdef SVG2_TRACE_PRINT
         if (n_done == 0 && blockIdx.x == 0 && lane == 0) trace_T = T;
+#endif
         ++n_done;
       }
     } else if (warp == kWarpMma) {
@@ -453,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, s2);
         tmem_ld32(tS + 96, s3);
         tmem_wait_ld();
+        if ((warp & 3) == 0) TRACE(10 + g, t);
         if (p.debug_mode == 1) {  // measurement: the MMA/TMA pipeline without the softmax math
           uint32_t z[16];
 #pragma unroll
@@ -505,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_used = m_new;
         }
+        if ((warp & 3) == 0) TRACE(12 + g, t);
         // p = 2^(s * scale*log2e - m): FFMA2 on pairs, MUFU ex2 per element, FADD2 row sums, bf16x2 packs
         const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m_used, -m_used);
         uint64_t lsum2 = f2(0.f, 0.f);
@@ -530,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         exp_store(s1, 1);
         exp_store(s2, 2);
         exp_store(s3, 3);
+        if ((warp & 3) == 0) TRACE(14 + g, t);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
