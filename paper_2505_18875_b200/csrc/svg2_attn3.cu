@@ -792,6 +792,7 @@ cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void
     return launch_varblock_attention_v2(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
   if (variant == 4)
     return launch_varblock_attention_v4(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
+
   return launch_varblock_attention_v3(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
 }
 
