@@ -217,11 +217,28 @@ def run_ours(args, wl):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # SVG2_BENCH_DEVICE / SVG2_DIST_BACKEND=gloo exist to exercise the multi-rank path on a single GPU (tests only);
+    # a real run uses one GPU per rank and NCCL
+    local_dev = int(os.environ.get("SVG2_BENCH_DEVICE", local))
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SVG2_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     svg2.load_library()
+
+    def reduce_scalar(x, op):
+        """max / sum over ranks (device time is the max over ranks); CPU tensor on a CPU-only backend."""
+        if world == 1:
+            return x
+        on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+        t = torch.tensor([x], device=on, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
     top_p = args.top_p if args.top_p is not None else wl.top_p
     from paper_2505_18875_b200.dist import head_range, head_to_seq, seq_to_head
     h0, h1 = head_range(wl.H, rank, world)
@@ -287,13 +304,9 @@ def run_ours(args, wl):
         torch.cuda.synchronize()
     total_ms = start.elapsed_time(stop)
     t_local = total_ms / args.steps
+    t_call = reduce_scalar(t_local, "max")
     if world > 1:
-        t = torch.tensor([t_local], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_call = float(t.item())
         dist.barrier()
-    else:
-        t_call = t_local
     for nm in stage_ms:
         stage_ms[nm] /= args.steps
     # per-step time includes a host sync per step for the stage events; report the pure back-to-back call too
@@ -305,21 +318,11 @@ def run_ours(args, wl):
     stop2.record()
     torch.cuda.synchronize()
     t_b2b_local = start2.elapsed_time(stop2) / args.steps
-    if world > 1:
-        t = torch.tensor([t_b2b_local], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_b2b = float(t.item())
-    else:
-        t_b2b = t_b2b_local
+    t_b2b = reduce_scalar(t_b2b_local, "max")
     t_use = min(t_call, t_b2b)
 
     pairs_local = float(pairs.double().sum().item())
-    if world > 1:
-        pt = torch.tensor([pairs_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(pt)
-        pairs_total = float(pt.item())
-    else:
-        pairs_total = pairs_local
+    pairs_total = reduce_scalar(pairs_local, "sum")
     density = pairs_total / (B * wl.H * N * N)
     dense_flops = 4.0 * N * N * d * B * wl.H
     value = dense_flops / (t_use * 1e-3) / 1e12
@@ -361,10 +364,7 @@ def run_ours(args, wl):
         e3.record()
         torch.cuda.synchronize()
         te = s3.elapsed_time(e3) / args.steps
-        if world > 1:
-            t = torch.tensor([te], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+        te = reduce_scalar(te, "max")
         nbytes = B * Hl * N * d * 2
         e2e = {"value": dense_flops / (te * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": te,
                "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world,

@@ -21,6 +21,17 @@ def head_range(H: int, rank: int, world: int):
     return rank * per, (rank + 1) * per
 
 
+def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group=None) -> None:
+    """all_to_all_single; with a CPU-only backend (gloo, used to exercise the multi-rank path on one GPU) the CUDA
+    buffers are staged through host memory."""
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        r = torch.empty_like(recv, device="cpu")
+        dist.all_to_all_single(r, send.cpu(), group=group)
+        recv.copy_(r)
+    else:
+        dist.all_to_all_single(recv, send, group=group)
+
+
 def seq_to_head(x: torch.Tensor, group=None) -> torch.Tensor:
     """[B, N/P, H, d] (this rank's token chunk, all heads) -> [B, H/P, N, d] (all tokens, this rank's heads)."""
     world = dist.get_world_size(group)
@@ -28,7 +39,7 @@ def seq_to_head(x: torch.Tensor, group=None) -> torch.Tensor:
     hp = H // world
     send = x.reshape(B, n, world, hp, d).permute(2, 0, 1, 3, 4).contiguous()  # [P(dest), B, n, H/P, d]
     recv = torch.empty_like(send)                                             # [P(src = token chunk), B, n, H/P, d]
-    dist.all_to_all_single(recv, send, group=group)
+    _all_to_all(recv, send, group)
     return recv.permute(1, 3, 0, 2, 4).reshape(B, hp, world * n, d).contiguous()
 
 
@@ -39,7 +50,7 @@ def head_to_seq(y: torch.Tensor, group=None) -> torch.Tensor:
     n = N // world
     send = y.reshape(B, hp, world, n, d).permute(2, 0, 3, 1, 4).contiguous()  # [P(dest = token chunk), B, n, H/P, d]
     recv = torch.empty_like(send)                                              # [P(src = head group), B, n, H/P, d]
-    dist.all_to_all_single(recv, send, group=group)
+    _all_to_all(recv, send, group)
     return recv.permute(1, 2, 0, 3, 4).reshape(B, n, world * hp, d).contiguous()
 
 
