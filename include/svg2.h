@@ -162,7 +162,8 @@ SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const
 
 /* ---- The fused call on HOST buffers (offload / end-to-end use).  Qh, Kh, Vh [B,H,N,d] bf16 and Oh [B,H,Nq,d] bf16
  * in host memory (page-locked for the copies to overlap; pageable memory works but serialises).  Same math and
- * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (6 by default): the copy of
+ * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (small first and last ones,
+ * then 6 equal middle ones): the copy of
  * chunk c+1 to the device and of chunk c-1 back to the host overlap the computation of chunk c (internal streams,
  * double-buffered device staging in the workspace, SVG2_ENTRY_SPARSE_ATTENTION_HOST).  The centroid caches and
  * selected_pairs are DEVICE buffers as in svg2_sparse_attention.  The work is ordered after the work already queued

@@ -11,7 +11,8 @@ using namespace svg2;
 namespace {
 
 constexpr long long kMaxN = 1ll << 24;
-constexpr int kHostChunks = 6;  // head chunks of the host-buffer pipeline (measured e2e 77 / 69 / 67 / 65 / 67 ms at 2 / 3 / 4 / 6 / 8 chunks, HunyuanVideo; env SVG2_HOST_CHUNKS overrides)
+constexpr int kMaxHostChunks = 64;
+constexpr int kHostChunks = 6;  // middle chunks of the host pipeline (e2e, HunyuanVideo: 67.1 / 63.4 / 63.1 / 61.7 ms with 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; env SVG2_HOST_CHUNKS / SVG2_HOST_RAMP override)
 
 svg2_status_t check_device() {
   int dev = 0, major = 0, minor = 0;
@@ -147,19 +148,51 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
 
 // Host-buffer pipeline (svg2_sparse_attention_host): heads in chunks, double-buffered device staging.
 struct HostPlan {
-  int BH, hc, nchunks;
+  int BH, hc, nchunks;      // hc = the largest chunk (staging size)
+  int start[kMaxHostChunks + 1];  // chunk c = heads [start[c], start[c+1])
 };
+// Head chunks of the host pipeline.  Only the first chunk's upload and the last chunk's download are not overlapped
+// with computation, so the chunks ramp up 1, 2 heads at the start and down 2, 1 at the end around equal middle
+// chunks (kHostChunks of them); small problems get one chunk per head.
 HostPlan host_plan(const svg2_dims_t& dm) {
   static const int chunks_env = [] {
     const char* e = getenv("SVG2_HOST_CHUNKS");
     return e ? atoi(e) : 0;
   }();
+  static const int ramp_env = [] {
+    const char* e = getenv("SVG2_HOST_RAMP");
+    return e ? atoi(e) : 1;
+  }();
   HostPlan p;
   p.BH = dm.B * dm.H;
-  int chunks = chunks_env > 0 ? chunks_env : kHostChunks;
-  chunks = chunks < p.BH ? chunks : p.BH;
-  p.hc = (p.BH + chunks - 1) / chunks;
-  p.nchunks = (p.BH + p.hc - 1) / p.hc;
+  int sizes[kMaxHostChunks], n = 0;
+  const int mid_want = chunks_env > 0 ? chunks_env : kHostChunks;
+  const int mid_chunks = mid_want < kMaxHostChunks - 4 ? mid_want : kMaxHostChunks - 4;
+  int rest = p.BH;
+  const int ramp[2] = {1, 2};
+  const bool use_ramp = ramp_env != 0 && p.BH >= 2 * (ramp[0] + ramp[1]) + mid_chunks;
+  if (use_ramp) {
+    sizes[n++] = ramp[0];
+    sizes[n++] = ramp[1];
+    rest -= 2 * (ramp[0] + ramp[1]);
+  }
+  const int m = rest < mid_chunks ? (rest > 0 ? rest : 1) : mid_chunks;
+  for (int i = 0; i < m && rest > 0; ++i) {  // equal middle chunks (the first ones one head larger if uneven)
+    const int sz = rest / (m - i) + (rest % (m - i) ? 1 : 0);
+    sizes[n++] = sz;
+    rest -= sz;
+  }
+  if (use_ramp) {
+    sizes[n++] = ramp[1];
+    sizes[n++] = ramp[0];
+  }
+  p.nchunks = n;
+  p.hc = 1;
+  p.start[0] = 0;
+  for (int c = 0; c < n; ++c) {
+    p.start[c + 1] = p.start[c] + sizes[c];
+    p.hc = sizes[c] > p.hc ? sizes[c] : p.hc;
+  }
   return p;
 }
 struct HostWs {
@@ -397,7 +430,7 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, start, 0);
   const size_t qrow = size_t(dm.Nq) * dm.d * 2, krow = size_t(dm.Nk) * dm.d * 2;  // bytes per head
   for (int ci = 0; e == cudaSuccess && ci < n; ++ci) {
-    const int bh0 = ci * plan.hc, nh = plan.BH - bh0 < plan.hc ? plan.BH - bh0 : plan.hc, slot = ci & 1;
+    const int bh0 = plan.start[ci], nh = plan.start[ci + 1] - bh0, slot = ci & 1;
     cudaEvent_t in = ev[3 * ci], done = ev[3 * ci + 1], out = ev[3 * ci + 2];
     if (ci >= 2) e = cudaStreamWaitEvent(sin, ev[3 * (ci - 2) + 1], 0);  // slot's inputs consumed
     if (e == cudaSuccess)
