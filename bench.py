@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fp8", action="store_true", help="e4m3 P and V in the PV product (SVG2_FP8_PV, DESIGN R26)")
     ap.add_argument("--profile-once", action="store_true", help="one call only (for ncu)")
     return ap.parse_args()
 
@@ -256,11 +257,12 @@ def run_ours(args, wl):
     iters_w = args.iters_warm
 
     # cold call fills the centroid cache (the paper's first sparse step), then warm calls
-    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, top_p)
+    fp8 = bool(args.fp8)
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, top_p, fp8=fp8)
     cq, ck = ex["q_centroids"], ex["k_centroids"]
     torch.cuda.synchronize()
     if args.profile_once:
-        O, pairs, _ = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True)
+        O, pairs, _ = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, fp8=fp8)
         torch.cuda.synchronize()
         print(json.dumps({"profile_once": True, "density": float(pairs.double().sum()) / (B * Hl * N * N)}))
         return
@@ -272,7 +274,8 @@ def run_ours(args, wl):
             Qh, Kh, Vh = seq_to_head(Qs), seq_to_head(Ks), seq_to_head(Vs)
         else:
             Qh, Kh, Vh = Q, K, V
-        Oh, pr, _ = svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, events=events)
+        Oh, pr, _ = svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, events=events,
+                                          fp8=fp8)
         if world > 1:
             return head_to_seq(Oh), pr
         return Oh, pr
@@ -351,7 +354,7 @@ def run_ours(args, wl):
 
         def e2e_step():
             svg2.sparse_attention_host(pinned[0], pinned[1], pinned[2], wl.Cq, wl.Ck, iters_w, top_p, qc_e, kc_e,
-                                       warm=True, out=out_host)
+                                       warm=True, out=out_host, fp8=fp8)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -385,7 +388,7 @@ def run_ours(args, wl):
     # outside the timed region (this rank's heads): Q tiles of 128 rows per query cluster; key stream = runs of
     # adjacent selected key clusters, each padded to whole 8-row groups, the stream rounded up to 16 keys (DESIGN 6)
     _, _, dx = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, iters_w, top_p, cq.clone(), ck.clone(), warm=True,
-                                     debug=True)
+                                     debug=True, fp8=fp8)
     q_off = dx["q_offsets"].cpu().numpy().astype(np.int64).reshape(-1, wl.Cq + 1)
     k_off = dx["k_offsets"].cpu().numpy().astype(np.int64).reshape(-1, wl.Ck + 1)
     msk = dx["mask"].cpu().numpy().astype(bool).reshape(-1, wl.Cq, wl.Ck)
@@ -403,15 +406,15 @@ def run_ours(args, wl):
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_oracle_sample(wl, rows=4096, iters=iters_w, heads=2)
-    launches = svg2.launch_count(B, Hl, N, N, d, wl.Cq, wl.Ck, iters_w, top_p, True) * args.steps
+    launches = svg2.launch_count(B, Hl, N, N, d, wl.Cq, wl.Ck, iters_w, top_p, True, fp8=fp8) * args.steps
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_use, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16",
+            "vs_baseline": None, "dtype": "bf16 + e4m3 PV" if fp8 else "bf16",
             "data": "synthetic (svg2-synth v1: seeded Voronoi-group Q/K/V, bf16, shapes of the named workload)",
             "config": {"workload": wl.name, "B": B, "H": wl.H, "N": N, "d": d, "Cq": wl.Cq, "Ck": wl.Ck,
-                       "top_p": top_p, "kmeans_iters": iters_w, "warm_start": True,
+                       "top_p": top_p, "kmeans_iters": iters_w, "warm_start": True, "pv": "e4m3" if fp8 else "bf16",
                        "parallelism": f"head-parallel x{world}" + (" + Ulysses all-to-all" if world > 1 else ""),
                        "l2": "inputs larger than L2 (Q+K+V = %.2f GB > 126 MB)" % (3 * B * wl.H * N * d * 2 / 1e9)},
             "density": density, "ms_per_call": t_use, "ms_per_call_with_stage_events": t_call,

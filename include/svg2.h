@@ -66,13 +66,16 @@ typedef struct {
                                  DESIGN.md R25: Philox4x32-10 keyed (seed, 2*(b*H+h) + role), role 0 = Q, 1 = K;
                                  picks reproducible bit for bit.  Ignored with SVG2_WARM_START.  Costs C passes over
                                  X (the expense the centroid cache avoids). */
+#define SVG2_FP8_PV 4u /* the "+FP8" variant as DESIGN.md R26 reads it: P and V enter the PV
+                          product as e4m3 (V with a per-(b,h) scale 448 / max|V|, P unscaled), fp32 accumulation;
+                          QK^T, the softmax and the output stay bf16 / fp32.  d = 128 only. */
 
 typedef struct {
   int32_t Cq, Ck;  /* query / key cluster counts (paper default 100 / 500) */
   int32_t iters;   /* Lloyd iterations, exactly (R3) */
   double top_p;    /* top-p target in (0, 1] */
   float scale;     /* softmax scale; 0 => 1/sqrt(d) */
-  uint32_t flags;  /* SVG2_WARM_START | SVG2_INIT_KMEANSPP */
+  uint32_t flags;  /* SVG2_WARM_START | SVG2_INIT_KMEANSPP | SVG2_FP8_PV */
   uint32_t seed;   /* k-means++ generator seed (R25); unused otherwise */
 } svg2_config_t;
 

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("SVG2_LIBRARY", os.path.join(_HERE, "libsvg2.so"))
 
 SVG2_WARM_START = 1
 SVG2_INIT_KMEANSPP = 2  # cold init by k-means++ seeding (generator DESIGN R25)
+SVG2_FP8_PV = 4  # e4m3 P and V in the PV product (DESIGN R26), d = 128
 (ENTRY_KMEANS, ENTRY_PERMUTE, ENTRY_SELECT_TOPP, ENTRY_VARBLOCK_ATTENTION, ENTRY_UNPERMUTE, ENTRY_SPARSE_ATTENTION,
  ENTRY_SPARSE_ATTENTION_HOST) = range(7)
 STATUS = ["SVG2_OK", "SVG2_ERR_NULL_POINTER", "SVG2_ERR_INVALID_SHAPE", "SVG2_ERR_INVALID_PARAM",
@@ -245,15 +246,16 @@ def unpermute(Op, perm):
     return O
 
 
-def launch_count(B, H, Nq, Nk, d, Cq, Ck, iters, top_p, warm, init: str = "strided") -> int:
+def launch_count(B, H, Nq, Nk, d, Cq, Ck, iters, top_p, warm, init: str = "strided", fp8: bool = False) -> int:
     lib = load_library()
-    cfg = Config(Cq, Ck, iters, top_p, 0.0, SVG2_WARM_START if warm else _cold_flags(init), 0)
+    flags = (SVG2_WARM_START if warm else _cold_flags(init)) | (SVG2_FP8_PV if fp8 else 0)
+    cfg = Config(Cq, Ck, iters, top_p, 0.0, flags, 0)
     return int(lib.svg2_sparse_attention_launch_count(Dims(B, H, Nq, Nk, d), ctypes.byref(cfg)))
 
 
 def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_centroids=None, k_centroids=None,
                      warm: bool = False, scale: float = 0.0, debug: bool = False, events=None, out=None,
-                     init: str = "strided", seed: int = 0):
+                     init: str = "strided", seed: int = 0, fp8: bool = False):
     """The fused SVG2 call.  Q, K, V [B,H,N,d] bf16 CUDA.  q_centroids [B,H,Cq,d] / k_centroids [B,H,Ck,d] f32 are
     the centroid caches (read iff warm, always written).  Cold calls start k-means from `init` ("strided" or
     "kmeans++" with `seed`, R25).  Returns (O, selected_pairs, extras) where extras holds
@@ -274,7 +276,8 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
     _need(k_centroids, torch.float32, "k_centroids", 4)
     O = out if out is not None else torch.empty_like(Q)
     pairs = torch.empty(B, H, dtype=torch.int64, device=dev)
-    cfg = Config(Cq, Ck, iters, top_p, scale, SVG2_WARM_START if warm else _cold_flags(init), seed)
+    flags = (SVG2_WARM_START if warm else _cold_flags(init)) | (SVG2_FP8_PV if fp8 else 0)
+    cfg = Config(Cq, Ck, iters, top_p, scale, flags, seed)
     dims = Dims(B, H, Nq, Nk, d)
     # 0 = invalid arguments: still call the ABI so the caller gets its precise status code
     nbytes = int(lib.svg2_workspace_size(ENTRY_SPARSE_ATTENTION, dims, ctypes.byref(cfg)))
@@ -310,7 +313,7 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
 
 def sparse_attention_host(Qh, Kh, Vh, Cq: int, Ck: int, iters: int, top_p: float, q_centroids=None,
                           k_centroids=None, warm: bool = False, scale: float = 0.0, out=None, init: str = "strided",
-                          seed: int = 0, device=None):
+                          seed: int = 0, device=None, fp8: bool = False):
     """The fused call on HOST tensors (svg2_sparse_attention_host): Qh, Kh, Vh [B,H,N,d] bf16 CPU tensors (pin them
     for overlapped copies), output a bf16 CPU tensor (`out`, else a new pinned one).  The library streams head chunks
     to the device, computes and copies back with the transfers overlapping the computation.  Centroid caches and
@@ -333,7 +336,8 @@ def sparse_attention_host(Qh, Kh, Vh, Cq: int, Ck: int, iters: int, top_p: float
     _need(k_centroids, torch.float32, "k_centroids", 4)
     O = out if out is not None else torch.empty((B, H, Nq, d), dtype=torch.bfloat16).pin_memory()
     pairs = torch.empty(B, H, dtype=torch.int64, device=dev)
-    cfg = Config(Cq, Ck, iters, top_p, scale, SVG2_WARM_START if warm else _cold_flags(init), seed)
+    flags = (SVG2_WARM_START if warm else _cold_flags(init)) | (SVG2_FP8_PV if fp8 else 0)
+    cfg = Config(Cq, Ck, iters, top_p, scale, flags, seed)
     dims = Dims(B, H, Nq, Nk, d)
     nbytes = int(lib.svg2_workspace_size(ENTRY_SPARSE_ATTENTION_HOST, dims, ctypes.byref(cfg)))
     ws = _workspace(max(nbytes, 256), dev)

@@ -110,6 +110,9 @@ cudaError_t launch_stable_sort(const int32_t* labels, int BH, int N, int C, Sort
 cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const void* X0, void* X0p,
                                const void* X1, void* X1p, cudaStream_t s);
 cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int N, int d, void* O, cudaStream_t s);
+// FP8 PV: per-head |x| max (amax, f32 bits) and the gather of X[perm] rounded to e4m3 with scale 448 / amax
+cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, const void* X, void* Xq, uint32_t* amax,
+                                    cudaStream_t s);
 // k-means cold-start options (DESIGN R2, R25): strided rows, or k-means++ with the R25 generator
 struct KmeansInit {
   bool kmeanspp = false;
@@ -127,7 +130,8 @@ cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_off
                                   int Nq, int Nk, int Cq, int Ck, AttnWs ws, cudaStream_t s);
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk,
                                       int d, int Cq, int Ck, float scale, const int32_t* q_perm, void* O,
-                                      float* lse, AttnWs ws, cudaStream_t s);
+                                      float* lse, AttnWs ws, cudaStream_t s,
+                                      const uint32_t* v_amax = nullptr);
 int kmeans_launch_count(int iters, bool warm);
 cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
                             float* cent, void* ws, cudaStream_t s);

@@ -48,6 +48,7 @@ struct FusedWs {
   int32_t *lab_q, *lab_k, *perm_q, *perm_k, *off_q, *off_k, *size_q, *size_k;
   void *Qp, *Kp, *Vp;
   uint8_t* mask;
+  uint32_t* v_amax;  // FP8 PV: per-head max |V| (f32 bits)
   KmeansWs km;
   AttnWs attn;
 };
@@ -67,6 +68,7 @@ FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) 
   w.Kp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.Vp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.mask = c.take<uint8_t>(BH * cfg.Cq * cfg.Ck);
+  w.v_amax = c.take<uint32_t>(BH);
   // k-means scratch is reused by the Q and the K role (same stream, sequential): carve the larger one
   Carver probe_q(nullptr), probe_k(nullptr);
   carve_kmeans(probe_q, int(BH), dm.Nq, cfg.Cq);
@@ -89,7 +91,8 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
   if (cfg->iters < 1) return SVG2_ERR_INVALID_PARAM;
   if (!(cfg->top_p > 0.0 && cfg->top_p <= 1.0)) return SVG2_ERR_INVALID_PARAM;
   if (!(cfg->scale >= 0.f) || std::isinf(cfg->scale)) return SVG2_ERR_INVALID_PARAM;
-  if (cfg->flags & ~(SVG2_WARM_START | SVG2_INIT_KMEANSPP)) return SVG2_ERR_INVALID_PARAM;
+  if (cfg->flags & ~(SVG2_WARM_START | SVG2_INIT_KMEANSPP | SVG2_FP8_PV)) return SVG2_ERR_INVALID_PARAM;
+  if ((cfg->flags & SVG2_FP8_PV) && dm.d != 128) return SVG2_ERR_INVALID_PARAM;
   return SVG2_OK;
 }
 
@@ -129,7 +132,10 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
                       w.off_k, w.km, s, nullptr, init_k);
   mark(2);
   if (e == cudaSuccess) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
-  if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, V, w.Vp, s);
+  const bool fp8 = (cfg->flags & SVG2_FP8_PV) != 0;
+  if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, fp8 ? nullptr : V, w.Vp, s);
+  // FP8 PV (R26): V' in e4m3 with a per-head scale, written into the first half of the bf16 V' buffer
+  if (e == cudaSuccess && fp8) e = launch_gather_rows_e4m3(w.perm_k, BH, dm.Nk, dm.d, V, w.Vp, w.v_amax, s);
   mark(3);
   if (e == cudaSuccess)
     e = launch_select_topp(q_centroids, k_centroids, w.size_q, w.size_k, BH, cfg->Cq, cfg->Ck, dm.d, scale,
@@ -140,7 +146,7 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   mark(5);
   if (e == cudaSuccess)
     e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, cfg->Cq, cfg->Ck, scale, w.perm_q, O,
-                                  nullptr, w.attn, s);
+                                  nullptr, w.attn, s, fp8 ? w.v_amax : nullptr);
   mark(6);
   mark(7);
   return e;
@@ -373,6 +379,7 @@ int32_t svg2_sparse_attention_launch_count(svg2_dims_t dm, const svg2_config_t* 
   if (!cfg) return 0;
   const bool warm = cfg->flags & SVG2_WARM_START;
   int n = 2 * kmeans_launch_count(cfg->iters, warm) + 2 /*gathers*/ + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+  if (cfg->flags & SVG2_FP8_PV) n += 2;  // |V| max per head + the e4m3 gather
   if (!warm && (cfg->flags & SVG2_INIT_KMEANSPP))
     n += kmeanspp_launch_count(dm.B * dm.H, dm.Nq, dm.d) + kmeanspp_launch_count(dm.B * dm.H, dm.Nk, dm.d) - 2;
   return n;

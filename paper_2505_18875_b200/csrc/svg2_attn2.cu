@@ -87,6 +87,7 @@ struct Params {
   int Nq;
   float scale_log2;
   float rescale_thr;  // kRescaleThreshold unless overridden
+  const uint32_t* v_amax;  // kFp8: per-head max |V| (f32 bits); O is scaled by amax / 448 in the epilogue
   int debug_mode;  // measurement only (env SVG2_DEBUG_MODE): 1 = softmax skips max/exp (P = 0), 2 = cycle trace
 };
 
@@ -114,7 +115,7 @@ constexpr int kTraceTiles = 48, kTraceEvents = 16;
 // boxes covering it.  The stage's mbarrier receives ngt x 8 rows x D x 2 bytes.
 template <int D>
 __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* stage, uint64_t* bar, int ngt, int lane,
-                                             int2 gw) {
+                                             int2 gw, int nblk = Cfg<D>::kBlocks) {
   using C = Cfg<D>;
   const int prev_row = __shfl_up_sync(0xffffffffu, gw.x, 1);
   const int prev_nv = __shfl_up_sync(0xffffffffu, gw.y, 1);
@@ -129,7 +130,7 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
     while (len > 0) {
       const int kind = 31 - __clz(min(len, 16));  // largest power of two <= len, capped at 16 groups (128 rows)
       const int pw = 1 << kind;
-      for (int b = 0; b < C::kBlocks; ++b)
+      for (int b = 0; b < nblk; ++b)  // 128-byte column blocks (64 bf16, or all 128 e4m3 of a V row)
         tma_load_2d(stage + b * C::kBlockBytes + pos * 1024, &maps[kind], bar, 64 * b, row);
       pos += pw;
       len -= pw;
@@ -141,7 +142,9 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
 // kPoly: in every 16-pair chunk of a row's 128 exponentials, kPoly pairs take 2^x on the FMA/ALU pipes (ex2_poly2)
 // instead of MUFU, which otherwise bounds the softmax (16 ex2/clk/SM; tools/xu_micro.cu).  Env SVG2_EXP_POLY
 // (0, 2, 4, 6, 8, 10) selects the split for measurements.
-template <int D, int kPoly>
+// kFp8: the FP8 PV path (DESIGN R26) — V' arrives in e4m3 (scale 448 / amax per head), P is packed to e4m3 in
+// TMEM and PV runs as kind::f8f6f4 MMAs (K = 32 keys each, half the instructions of bf16); d = 128 only.
+template <int D, int kPoly, bool kFp8 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_varblock_attn(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ KVMaps kv, const Params p) {
   using C = Cfg<D>;
@@ -182,6 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == kWarpTmem) tmem_alloc<512>(&tmem_slot);
+  if (kFp8) {  // a tile of 16 (mod 32) keys ends in a K = 32 step whose last 16 V rows are stale: keep them finite
+    for (int i = threadIdx.x; i < int(kStages * C::kTileBytes / 16); i += kThreads)
+      reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
+    fence_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -235,9 +243,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           load_kv_tile<D>(kv.k, sK + ks * C::kTileBytes, &bars.k_full[ks], ngt, lane, gw);
           TRACE(8, t);
           mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
-          if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], bytes);
+          if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], kFp8 ? uint32_t(ngt) * 8u * D : bytes);
           __syncwarp();
-          load_kv_tile<D>(kv.v, sV + ks * C::kTileBytes, &bars.v_full[ks], ngt, lane, gw);
+          load_kv_tile<D>(kv.v, sV + ks * C::kTileBytes, &bars.v_full[ks], ngt, lane, gw, kFp8 ? 1 : C::kBlocks);
           TRACE(9, t);
           gw = gw_next;
           if (++ks == kStages) {
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       //   PV_a(t), S_a(t+1) | PV_b(t), S_b(t+1)  -- softmax of tile a overlaps tile b's MMAs and vice versa.
       uint32_t qph = 0, ks = 0, kph = 0, vs = 0, vph = 0, islot = 0, iph = 0;
       uint32_t oeph[2] = {0, 0}, pph[2] = {0, 0};
-      const uint32_t idesc_pv = idesc_bf16_f32(128, D, true);
+      const uint32_t idesc_pv = kFp8 ? idesc_e4m3_f32_bmn(128, D) : idesc_bf16_f32(128, D, true);
       const uint64_t dq0 = desc_kmajor_sw128(smem_u32(sQ)), dq1 = desc_kmajor_sw128(smem_u32(sQ + C::kTileBytes));
       const uint64_t dk0 = desc_kmajor_sw128(smem_u32(sK)), dk1 = desc_kmajor_sw128(smem_u32(sK + C::kTileBytes));
       const uint64_t dv0 = desc_mnmajor_sw128(smem_u32(sV), C::kBlockBytes);
@@ -288,12 +296,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         auto issue_pv = [&](int t, int g, uint32_t vstage, bool first) {
-          const int ksteps = int(tile_n(t)) / 16;
           const uint64_t vd = vstage ? dv1 : dv0;
           const uint32_t ps = tmem + C::col_s(g), d = tmem + C::col_o(g);
+          if (kFp8) {  // K = 32 keys per MMA: 8 TMEM columns of e4m3 P, 32 V rows (4 KB) of the stage
+            const int ksteps = (int(tile_n(t)) + 31) / 32;
 #pragma unroll 1
-          for (int k = 0; k < ksteps; ++k)
-            mma_ts_warp(d, ps + 8 * k, vd + uint64_t((k * 16 * 128) >> 4), idesc_pv, (!first || k > 0) ? 1u : 0u);
+            for (int k = 0; k < ksteps; ++k)
+              mma_ts8_warp(d, ps + 8 * k, vd + uint64_t((k * 32 * 128) >> 4), idesc_pv, (!first || k > 0) ? 1u : 0u);
+          } else {
+            const int ksteps = int(tile_n(t)) / 16;
+#pragma unroll 1
+            for (int k = 0; k < ksteps; ++k)
+              mma_ts_warp(d, ps + 8 * k, vd + uint64_t((k * 16 * 128) >> 4), idesc_pv, (!first || k > 0) ? 1u : 0u);
+          }
         };
         auto next_k = [&] {
           if (++ks == kStages) {
@@ -518,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t lsum2 = f2(0.f, 0.f);
         auto exp_store = [&](const uint32_t(&a)[32], int c) {
           uint32_t pk[16];
+          uint32_t pk8[8];  // kFp8: four e4m3 per column, key 4i + j in byte j
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             float x0, x1;
@@ -530,9 +546,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               p1 = ex2_approx(x1);
             }
             lsum2 = fadd2(lsum2, f2(p0, p1));
-            pk[e] = pack_bf16x2(p0, p1);
+            if (kFp8) {
+              const uint32_t h16 = pack_e4m3x2(p0, p1);
+              pk8[e >> 1] = (e & 1) ? (pk8[e >> 1] | (h16 << 16)) : h16;
+            } else {
+              pk[e] = pack_bf16x2(p0, p1);
+            }
           }
-          tmem_st16(tS + 16 * c, pk);
+          if (kFp8)
+            tmem_st8(tS + 8 * c, pk8);
+          else
+            tmem_st16(tS + 16 * c, pk);
         };
         exp_store(s0, 0);
         exp_store(s1, 1);
@@ -567,7 +591,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m = fmaxf(m_used, mlb.x);
         const float wa = ex2_approx(m_used - m), wb = ex2_approx(mlb.x - m);
         const float lt = l * wa + mlb.y * wb;
-        const float ca = wa / lt, cb = wb / lt;
+        const float vsc = kFp8 ? __uint_as_float(__ldg(p.v_amax + (it.w & kItemBhMask))) * (1.f / 448.f) : 1.f;
+        const float ca = wa / lt * vsc, cb = wb / lt * vsc;
         const long long row_flat = (long long)it.x + rloc;
         long long dst = row_flat;
         if (rloc < nrows && p.q_perm) dst = (long long)(it.w & kItemBhMask) * p.Nq + __ldg(p.q_perm + row_flat);
@@ -601,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++n_done;
         continue;
       }
-      const float inv_l = 1.f / l;
+      const float inv_l = (kFp8 ? __uint_as_float(__ldg(p.v_amax + (it.w & kItemBhMask))) * (1.f / 448.f) : 1.f) / l;
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
       if (rloc < nrows && p.q_perm) {
@@ -651,14 +676,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D>
 cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
-                     const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s) {
+                     const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s,
+                     const uint32_t* v_amax = nullptr) {
+  const bool fp8 = v_amax != nullptr;
+  if (fp8 && D != 128) return cudaErrorNotSupported;
   CUtensorMap mq;
   KVMaps kv;
   if (!make_tmap_bf16(&mq, Qp, uint64_t(BH) * Nq, D, 128)) return cudaErrorInvalidValue;
-  for (int k = 0; k < kBoxKinds; ++k)
-    if (!make_tmap_bf16(&kv.k[k], Kp, uint64_t(BH) * Nk, D, 8u << k) ||
-        !make_tmap_bf16(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k))
-      return cudaErrorInvalidValue;
+  for (int k = 0; k < kBoxKinds; ++k) {
+    const bool okv = fp8 ? make_tmap_u8(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k)
+                         : make_tmap_bf16(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k);
+    if (!make_tmap_bf16(&kv.k[k], Kp, uint64_t(BH) * Nk, D, 8u << k) || !okv) return cudaErrorInvalidValue;
+  }
   Params p;
   p.items = ws.items;
   p.n_items = ws.n_items;
@@ -682,6 +711,7 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
     return e ? float(atof(e)) : kRescaleThreshold;
   }();
   p.rescale_thr = rescale_thr;
+  p.v_amax = v_amax;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -693,6 +723,12 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes);
     kernel<<<sms, kThreads, Cfg<D>::kSmemBytes, s>>>(mq, kv, p);
   };
+  if constexpr (D == 128) {
+    if (fp8) {
+      launch(k_varblock_attn<D, kDefaultPoly, true>);
+      return cudaGetLastError();
+    }
+  }
   if (poly == 2) launch(k_varblock_attn<D, 2>);
   else if (poly == 4) launch(k_varblock_attn<D, 4>);
   else if (poly == 6) launch(k_varblock_attn<D, 6>);
@@ -706,11 +742,11 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
 
 cudaError_t launch_varblock_attention_v2(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                       int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
-                                      AttnWs ws, cudaStream_t s) {
+                                      AttnWs ws, cudaStream_t s, const uint32_t* v_amax) {
   (void)Cq;
   (void)Ck;
-  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s);
-  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s);
+  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s, v_amax);
+  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s, v_amax);
 }
 
 }  // namespace svg2

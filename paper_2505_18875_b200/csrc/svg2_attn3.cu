@@ -774,7 +774,7 @@ cudaError_t launch_varblock_attention_v3(const void* Qp, const void* Kp, const v
 // svg2_attn2.cu: the 128-key-tile design (single S/P buffer per Q tile)
 cudaError_t launch_varblock_attention_v2(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                          int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
-                                         AttnWs ws, cudaStream_t s);
+                                         AttnWs ws, cudaStream_t s, const uint32_t* v_amax);
 cudaError_t launch_varblock_attention_v4(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                          int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
                                          AttnWs ws, cudaStream_t s);
@@ -783,13 +783,14 @@ cudaError_t launch_varblock_attention_v4(const void* Qp, const void* Kp, const v
 // measurements, kDefaultAttnVariant otherwise.
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                       int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
-                                      AttnWs ws, cudaStream_t s) {
+                                      AttnWs ws, cudaStream_t s, const uint32_t* v_amax) {
   static const int variant = [] {
     const char* e = getenv("SVG2_ATTN_VARIANT");
     return e ? atoi(e) : kDefaultAttnVariant;
   }();
-  if (variant == 2)
-    return launch_varblock_attention_v2(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
+  // the FP8 PV path (V' in e4m3, v_amax = per-head |V| max) exists in design v2 only
+  if (variant == 2 || v_amax)
+    return launch_varblock_attention_v2(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s, v_amax);
   if (variant == 4)
     return launch_varblock_attention_v4(Qp, Kp, Vp, BH, Nq, Nk, d, Cq, Ck, scale, q_perm, O, lse, ws, s);
 

@@ -33,4 +33,18 @@ inline bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, int d
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 8-bit elements (e4m3 V' of the FP8 PV path): rows of d bytes, boxes of d bytes x box_rows (one 128-byte swizzle
+// row per token for d = 128)
+inline bool make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t rows, int d, uint32_t box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {cuuint64_t(d), rows};
+  cuuint64_t gstr[1] = {cuuint64_t(d)};
+  cuuint32_t box[2] = {uint32_t(d), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), gdim, gstr, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace svg2

@@ -79,12 +79,16 @@ def test_validation_rejects_before_touching_the_device(lib):
                                      16, None) == 5
     # unknown flag bits -> SVG2_ERR_INVALID_PARAM; the k-means++ cold-start flag is accepted (then the fake pointers
     # fail the device check or later, never the parameter check)
-    cfg_flag = m.Config(8, 8, 1, 0.9, 0.0, 4)
+    cfg_flag = m.Config(8, 8, 1, 0.9, 0.0, 8)
     assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg_flag), fake, fake, fake, None, None,
                                      fake, 1 << 30, None) == 3
     cfg_pp = m.Config(8, 8, 1, 0.9, 0.0, m.SVG2_INIT_KMEANSPP, 7)
     assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg_pp), fake, fake, fake, None, None,
                                      fake, 1 << 30, None) not in (1, 2, 3, 4, 5)
+    # the FP8 PV path needs d = 128
+    cfg_fp8 = m.Config(8, 8, 1, 0.9, 0.0, m.SVG2_FP8_PV)
+    assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg_fp8), fake, fake, fake, None, None,
+                                     fake, 1 << 30, None) == 3
     # svg2_kmeans: role must be 0 (queries) or 1 (keys)
     assert lib.svg2_kmeans(fake, 1, 1, 256, 64, 8, 1, m.SVG2_INIT_KMEANSPP, 7, 2, fake, fake, fake, None, None, fake,
                            1 << 30, None) == 3

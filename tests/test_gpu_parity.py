@@ -428,3 +428,38 @@ def test_heads_are_independent_bitwise(svg2):
         assert torch.equal(Oh[0, 0], O[0, h]), f"head {h}"
         assert torch.equal(ph[0, 0], pairs[0, h])
         assert torch.equal(exh["q_centroids"][0, 0], ex["q_centroids"][0, h])
+
+
+FP8_REL, FP8_ABS, FP8_MEAN_REL = 2.0 ** -3, 2.0 ** -6, 2.0 ** -4
+
+
+@pytest.mark.parametrize("case", ["random", "hunyuan_rows"])
+def test_fp8_pv_within_e4m3_bound(svg2, oracle_mod, case):
+    """SVG2_FP8_PV (DESIGN R26): P and V enter PV rounded to e4m3 (relative error <= 2^-4 each for normal values).
+    To first order the output error of element (i, c) is then bounded by 2^-3 * sum_k p_ik |v_kc| (the oracle's
+    attention over |V| with the same selection), plus an absolute 2^-6 for e4m3 subnormals and the bf16 output;
+    on average the error stays within one e4m3 rounding of that magnitude (2^-4).  Same selection as the bf16 path
+    (the mask does not depend on PV)."""
+    if case == "random":
+        q, k, v = random_qkv(1, 2, 3000, 3000, 128, seed=61)
+        Cq, Ck, p, rows = 24, 48, 0.9, np.arange(0, 3000, 2)
+    else:
+        wl = svg2_synth.WORKLOADS["hunyuan720p"]
+        q, k, v = svg2_synth.generate(wl, heads=[0])
+        Cq, Ck, p = wl.Cq, wl.Ck, wl.top_p
+        rows = np.sort(np.random.default_rng(5).choice(wl.N, 400, replace=False))
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O8, pairs8, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, 3, p, debug=True, fp8=True)
+    O, pairs, _ = svg2.sparse_attention(Q, K, V, Cq, Ck, 3, p, fp8=False)
+    assert torch.equal(pairs8, pairs)
+    errs, mags = [], []
+    for h in range(Q.shape[1]):
+        lq, lk, m = (ex[key][0, h].cpu().numpy() for key in ("q_labels", "k_labels", "mask"))
+        Q64, K64, V64 = to_f64(Q)[0, h], to_f64(K)[0, h], to_f64(V)[0, h]
+        ref = oracle_mod.attention_rows(Q64, K64, V64, f32scale(128), rows=rows, lq=lq, lk=lk, mask=m)
+        mag = oracle_mod.attention_rows(Q64, K64, np.abs(V64), f32scale(128), rows=rows, lq=lq, lk=lk, mask=m)
+        err = np.abs(to_f64(O8)[0, h][rows] - ref)
+        assert np.all(err <= FP8_REL * mag + FP8_ABS), f"head {h}: worst excess {np.max(err - FP8_REL * mag):.3e}"
+        errs.append(err)
+        mags.append(mag)
+    assert np.concatenate(errs).mean() <= FP8_MEAN_REL * np.concatenate(mags).mean()
