@@ -342,7 +342,7 @@ def run_ours(args, wl):
                 "peak_source": f"{pk_src} bf16 sustained (cuBLAS 8192^3 back-to-back, MEASURED_PEAKS.json)"
                 + (" for QK^T, x2 (nominal fp8/bf16) for PV, harmonic mix" if fp8 else ""),
                 "algorithmic": "4*d*selected_pairs executed FLOPs per launch / event time of the launch"}
-    traffic_file = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
+    traffic_file = os.path.join(ROOT, "profiles", f"traffic_{wl.name}{'_fp8' if fp8 else ''}.json")
     if os.path.exists(traffic_file):
         try:
             roofline["traffic"] = json.load(open(traffic_file)).get("dram_bytes_per_launch")
