@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp8", action="store_true", help="e4m3 P and V in the PV product (SVG2_FP8_PV, DESIGN R26)")
+    ap.add_argument("--balance", action="store_true",
+                    help="N > 1: heads -> ranks by measured per-head time (dist.balanced_assignment), fixed after a "
+                         "calibration step")
     ap.add_argument("--profile-once", action="store_true", help="one call only (for ncu)")
     return ap.parse_args()
 
@@ -241,7 +244,8 @@ def run_ours(args, wl):
         return float(t.item())
 
     top_p = args.top_p if args.top_p is not None else wl.top_p
-    from paper_2505_18875_b200.dist import head_range, head_to_seq, seq_to_head
+    from paper_2505_18875_b200.dist import (balanced_assignment, head_range, head_to_seq, heads_to_seq, seq_to_head,
+                                            seq_to_heads)
     h0, h1 = head_range(wl.H, rank, world)
     Hl = h1 - h0
     # inputs: this rank's heads, full sequence (synthetic, seeded per head)
@@ -261,6 +265,36 @@ def run_ours(args, wl):
     O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, top_p, fp8=fp8)
     cq, ck = ex["q_centroids"], ex["k_centroids"]
     torch.cuda.synchronize()
+    assignment = None
+    if args.balance and world > 1:
+        # calibration: time each local head alone (warm), gather all heads' times, assign by LPT, keep it fixed
+        times = []
+        for hh in range(Hl):
+            sl = slice(hh, hh + 1)
+            Qh, Kh, Vh = (t[:, sl].contiguous() for t in (Q, K, V))
+            a, b = cq[:, sl].contiguous(), ck[:, sl].contiguous()
+            svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, a.clone(), b.clone(), warm=True, fp8=fp8)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(2):
+                svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, a.clone(), b.clone(), warm=True,
+                                      fp8=fp8)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 2)
+        on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+        mine_t = torch.tensor(times, dtype=torch.float64, device=on)
+        all_t = [torch.empty_like(mine_t) for _ in range(world)]
+        dist.all_gather(all_t, mine_t)
+        head_times = torch.cat(all_t).cpu().tolist()  # rank r holds heads [h0, h1) of the fixed split, in order
+        assignment = balanced_assignment(head_times, world)
+        Q, K, V = (seq_to_heads(t, assignment) for t in (Qs, Ks, Vs))
+        Hl = Q.shape[1]
+        if pinned is not None:
+            pinned = [t.cpu().pin_memory() for t in (Q, K, V)]
+        O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, top_p, fp8=fp8)  # caches of my heads
+        cq, ck = ex["q_centroids"], ex["k_centroids"]
+        torch.cuda.synchronize()
     if args.profile_once:
         O, pairs, _ = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, fp8=fp8)
         torch.cuda.synchronize()
@@ -270,12 +304,16 @@ def run_ours(args, wl):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
 
     def step(events=None):
-        if world > 1:
+        if assignment is not None:
+            Qh, Kh, Vh = (seq_to_heads(t, assignment) for t in (Qs, Ks, Vs))
+        elif world > 1:
             Qh, Kh, Vh = seq_to_head(Qs), seq_to_head(Ks), seq_to_head(Vs)
         else:
             Qh, Kh, Vh = Q, K, V
         Oh, pr, _ = svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, events=events,
                                           fp8=fp8)
+        if assignment is not None:
+            return heads_to_seq(Oh, assignment, wl.H), pr
         if world > 1:
             return head_to_seq(Oh), pr
         return Oh, pr
@@ -372,9 +410,9 @@ def run_ours(args, wl):
         torch.cuda.synchronize()
         te = s3.elapsed_time(e3) / args.steps
         te = reduce_scalar(te, "max")
-        nbytes = B * Hl * N * d * 2
+        nbytes = int(reduce_scalar(float(B * Hl * N * d * 2), "sum"))  # all ranks (uneven with --balance)
         e2e = {"value": dense_flops / (te * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": te,
-               "h2d_bytes_per_step": 3 * nbytes * world, "d2h_bytes_per_step": nbytes * world,
+               "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes,
                "api": "svg2_sparse_attention_host (C ABI, pinned host Q/K/V in, host O out)"}
 
     # ---- dense baseline (same box, same inputs)
@@ -382,7 +420,7 @@ def run_ours(args, wl):
     if not args.no_dense and rank == 0:
         best, res = dense_baseline(Q, K, V)
         if best:
-            t_dense = res[best] * world  # this rank's heads on one GPU; scale to the whole job on one GPU
+            t_dense = res[best] * wl.H / Hl  # this rank's heads on one GPU; scale to all heads on one GPU
             dense = {"best_backend": best, "ms_per_call_1gpu_all_heads": t_dense, "backends_ms_rank_heads": res,
                      "speedup_vs_dense": t_dense / (t_use * world) if world == 1 else None,
                      "inv_density": 1.0 / density if density > 0 else None,
@@ -419,12 +457,14 @@ def run_ours(args, wl):
             "data": "synthetic (svg2-synth v1: seeded Voronoi-group Q/K/V, bf16, shapes of the named workload)",
             "config": {"workload": wl.name, "B": B, "H": wl.H, "N": N, "d": d, "Cq": wl.Cq, "Ck": wl.Ck,
                        "top_p": top_p, "kmeans_iters": iters_w, "warm_start": True, "pv": "e4m3" if fp8 else "bf16",
-                       "parallelism": f"head-parallel x{world}" + (" + Ulysses all-to-all" if world > 1 else ""),
+                       "parallelism": f"head-parallel x{world}" + (" + Ulysses all-to-all" if world > 1 else "")
+                       + (" (heads balanced by measured time)" if assignment is not None else ""),
                        "l2": "inputs larger than L2 (Q+K+V = %.2f GB > 126 MB)" % (3 * B * wl.H * N * d * 2 / 1e9)},
             "density": density, "ms_per_call": t_use, "ms_per_call_with_stage_events": t_call,
             "stages_ms": stage_ms, "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
             "dense_baseline": dense, "cpu_baseline": cpu, "clocks": clocks.summary(),
             "attention_executed_tflops": achieved, "tile_work_multiplier": tile_work,
+            "head_assignment": assignment,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

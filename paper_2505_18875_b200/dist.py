@@ -54,6 +54,77 @@ def head_to_seq(y: torch.Tensor, group=None) -> torch.Tensor:
     return recv.permute(1, 2, 0, 3, 4).reshape(B, n, world * hp, d).contiguous()
 
 
+# ------------------------------------------------------------------ load balancing
+# Dynamic top-p gives every head its own density, so equal head counts per rank are not equal work.
+# balanced_assignment() gives each rank a set of heads with near-equal estimated cost (longest-processing-time-first,
+# deterministic); the uneven reshards below move each rank's token chunk to the owners of its heads and back.
+# The mapping is chosen once (e.g. from the first sparse step's per-head work) and kept, so centroid caches stay
+# resident on their rank.
+
+
+def balanced_assignment(costs, world: int):
+    """Heads -> ranks with near-equal total cost: heads in decreasing cost (ties: lower index first), each to the
+    least-loaded rank (ties: lower rank).  Returns a list of sorted head lists, one per rank."""
+    costs = [float(c) for c in costs]
+    order = sorted(range(len(costs)), key=lambda h: (-costs[h], h))
+    load = [0.0] * world
+    heads = [[] for _ in range(world)]
+    for h in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        heads[r].append(h)
+        load[r] += costs[h]
+    return [sorted(hs) for hs in heads]
+
+
+def makespan(costs, heads_per_rank):
+    """Largest per-rank total cost of an assignment."""
+    return max(sum(float(costs[h]) for h in hs) for hs in heads_per_rank)
+
+
+def seq_to_heads(x: torch.Tensor, heads_per_rank, group=None) -> torch.Tensor:
+    """Uneven Ulysses reshard: [B, N/P, H, d] (this rank's token chunk, all heads) -> [B, |A_r|, N, d] (all tokens of
+    the heads A_r = heads_per_rank[rank]).  Every head must appear in exactly one list."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    B, n, H, d = x.shape
+    send = torch.cat([x[:, :, hs].reshape(-1) for hs in heads_per_rank]).contiguous()
+    splits_out = [B * n * len(hs) * d for hs in heads_per_rank]
+    mine = heads_per_rank[rank]
+    recv = torch.empty(world * B * n * len(mine) * d, dtype=x.dtype, device=x.device)
+    _all_to_all_uneven(recv, send, [B * n * len(mine) * d] * world, splits_out, group)
+    # recv: [P(src = token chunk), B, n, |A_r|, d] -> [B, |A_r|, N, d]
+    return recv.view(world, B, n, len(mine), d).permute(1, 3, 0, 2, 4).reshape(B, len(mine), world * n, d).contiguous()
+
+
+def heads_to_seq(y: torch.Tensor, heads_per_rank, H: int, group=None) -> torch.Tensor:
+    """Inverse of seq_to_heads: [B, |A_r|, N, d] -> [B, N/P, H, d]."""
+    world = dist.get_world_size(group)
+    B, hr, N, d = y.shape
+    n = N // world
+    send = y.reshape(B, hr, world, n, d).permute(2, 0, 3, 1, 4).contiguous()  # [P(dest = token chunk), B, n, |A_r|, d]
+    recv = torch.empty(sum(B * n * len(hs) * d for hs in heads_per_rank), dtype=y.dtype, device=y.device)
+    _all_to_all_uneven(recv, send.reshape(-1), [B * n * len(hs) * d for hs in heads_per_rank],
+                       [B * n * hr * d] * world, group)
+    out = torch.empty(B, n, H, d, dtype=y.dtype, device=y.device)
+    off = 0
+    for hs in heads_per_rank:  # the part from rank q holds its heads A_q
+        size = B * n * len(hs) * d
+        out[:, :, hs] = recv[off:off + size].view(B, n, len(hs), d)
+        off += size
+    return out
+
+
+def _all_to_all_uneven(recv, send, in_splits_recv, out_splits_send, group=None):
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        r = torch.empty_like(recv, device="cpu")
+        dist.all_to_all_single(r, send.cpu(), output_split_sizes=in_splits_recv, input_split_sizes=out_splits_send,
+                               group=group)
+        recv.copy_(r)
+    else:
+        dist.all_to_all_single(recv, send, output_split_sizes=in_splits_recv, input_split_sizes=out_splits_send,
+                               group=group)
+
+
 class HeadParallelSVG2:
     """Sequence-parallel in, sequence-parallel out; SVG2 on this rank's heads in between."""
 

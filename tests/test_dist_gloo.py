@@ -66,3 +66,60 @@ def test_head_range_partition():
         assert covered == list(range(H))
     with pytest.raises(ValueError):
         head_range(24, 0, 5)
+
+
+def _worker_uneven(rank, world, port, B, N, H, d, heads_per_rank, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_18875_b200.dist import heads_to_seq, seq_to_heads
+        g = torch.Generator().manual_seed(99)
+        full = torch.randn(B, N, H, d, generator=g)
+        n = N // world
+        local_seq = full[:, rank * n:(rank + 1) * n].contiguous()
+        y = seq_to_heads(local_seq, heads_per_rank)
+        expect = full[:, :, heads_per_rank[rank]].permute(0, 2, 1, 3).contiguous()
+        ok1 = torch.equal(y, expect)
+        back = heads_to_seq(y * 2, heads_per_rank, H)
+        ok2 = torch.equal(back, local_seq * 2)
+        q.put((rank, ok1, ok2))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,heads_per_rank", [(2, [[0, 3, 4], [1, 2]]), (3, [[5], [0, 1, 2, 3], [4]])])
+def test_uneven_reshard_roundtrip(world, heads_per_rank):
+    """Balanced (uneven) head assignments: each rank receives all tokens of exactly its heads, and the way back
+    restores every head of its token chunk."""
+    B, N, H, d = 2, 12, sum(len(h) for h in heads_per_rank), 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_uneven, args=(r, world, port, B, N, H, d, heads_per_rank, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok1 and ok2 for _, ok1, ok2 in results), results
+
+
+def test_balanced_assignment_lpt():
+    from paper_2505_18875_b200.dist import balanced_assignment, makespan
+    costs = [10, 1, 9, 2, 8, 3, 7, 4]
+    a = balanced_assignment(costs, 2)
+    assert sorted(h for hs in a for h in hs) == list(range(8))
+    assert makespan(costs, a) == 22  # total 44: a perfect split exists and LPT finds it here
+    # never worse than the contiguous equal-count split, and within 4/3 of the lower bound (LPT guarantee)
+    rng = torch.Generator().manual_seed(3)
+    for world in (2, 4, 8):
+        c = (torch.rand(24, generator=rng) + 0.5).tolist()
+        lb = max(sum(c) / world, max(c))
+        a = balanced_assignment(c, world)
+        per = 24 // world
+        fixed = [list(range(r * per, (r + 1) * per)) for r in range(world)]
+        assert makespan(c, a) <= makespan(c, fixed) + 1e-12
+        assert makespan(c, a) <= 4.0 / 3.0 * lb + 1e-9
