@@ -35,7 +35,9 @@ namespace {
 // (internal names shared with svg2_attn3.cu live in this file's anonymous namespace)
 
 constexpr int kThreads = 384;
-constexpr int kStages = 2;
+constexpr int kStages = 2;     // K/V ring depth (bf16)
+constexpr int kStagesFp8 = 3;  // with e4m3 V tiles (16 KB) a third stage fits: prefetch two tiles ahead
+constexpr int kStagesMax = 3;
 constexpr int kGroupsPerTile = kKTile / 8;  // 16
 constexpr int kBoxKinds = 5;                // box heights 8, 16, 32, 64, 128 rows
 // Lazy rescale threshold (log2 units): O and l are rescaled only when a row's tile max exceeds the max in use by
@@ -58,6 +60,8 @@ struct Cfg {
   static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;
   static constexpr uint32_t kGroupBytes = 8 * 2 * D;   // 8 rows x D bf16
   static constexpr uint32_t kSmemBytes = (2 + 2 * kStages) * kTileBytes + 1024;
+  // FP8 PV: kStagesFp8 K tiles and kStagesFp8 half-size (e4m3) V tiles
+  static constexpr uint32_t kSmemBytesFp8 = (2 + kStagesFp8) * kTileBytes + kStagesFp8 * (kTileBytes / 2) + 1024;
   // TMEM columns: S of Q tile g at col_s(g) (P aliases it as bf16), O at col_o(g)
   __host__ __device__ static constexpr uint32_t col_s(int g) { return g ? 128u : 0u; }
   __host__ __device__ static constexpr uint32_t col_o(int g) { return g ? 384u : 256u; }
@@ -65,7 +69,7 @@ struct Cfg {
 
 struct Bars {
   uint64_t q_full, q_empty;
-  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+  uint64_t k_full[kStagesMax], k_empty[kStagesMax], v_full[kStagesMax], v_empty[kStagesMax];
   uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
   uint64_t item_full[2], item_empty[2];
 };
@@ -151,8 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                // [2][tile]
-  uint8_t* sK = smem + 2 * C::kTileBytes;            // [kStages][tile]
-  uint8_t* sV = sK + kStages * C::kTileBytes;        // [kStages][tile]
+  constexpr int kSt = kFp8 ? kStagesFp8 : kStages;                  // K/V ring depth
+  constexpr uint32_t kVTile = kFp8 ? C::kTileBytes / 2 : C::kTileBytes;  // one V stage (e4m3: 1 byte / element)
+  uint8_t* sK = smem + 2 * C::kTileBytes;            // [kSt][tile]
+  uint8_t* sV = sK + kSt * C::kTileBytes;            // [kSt][kVTile]
   __shared__ Bars bars;
   __shared__ uint32_t tmem_slot;
   __shared__ int4 item_slot[2];
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&mapQ);
     mbar_init(&bars.q_full, 1);
     mbar_init(&bars.q_empty, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(&bars.k_full[s], 1);
       mbar_init(&bars.k_empty[s], 1);
       mbar_init(&bars.v_full[s], 1);
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == kWarpTmem) tmem_alloc<512>(&tmem_slot);
   if (kFp8) {  // a tile of 16 (mod 32) keys ends in a K = 32 step whose last 16 V rows are stale: keep them finite
-    for (int i = threadIdx.x; i < int(kStages * C::kTileBytes / 16); i += kThreads)
+    for (int i = threadIdx.x; i < int(kSt * kVTile / 16); i += kThreads)
       reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
     fence_async_smem();
   }
@@ -245,10 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
           if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], kFp8 ? uint32_t(ngt) * 8u * D : bytes);
           __syncwarp();
-          load_kv_tile<D>(kv.v, sV + ks * C::kTileBytes, &bars.v_full[ks], ngt, lane, gw, kFp8 ? 1 : C::kBlocks);
+          load_kv_tile<D>(kv.v, sV + ks * kVTile, &bars.v_full[ks], ngt, lane, gw, kFp8 ? 1 : C::kBlocks);
           TRACE(9, t);
           gw = gw_next;
-          if (++ks == kStages) {
+          if (++ks == kSt) {
             ks = 0;
             kph ^= 1;
           }
@@ -267,9 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t oeph[2] = {0, 0}, pph[2] = {0, 0};
       const uint32_t idesc_pv = kFp8 ? idesc_e4m3_f32_bmn(128, D) : idesc_bf16_f32(128, D, true);
       const uint64_t dq0 = desc_kmajor_sw128(smem_u32(sQ)), dq1 = desc_kmajor_sw128(smem_u32(sQ + C::kTileBytes));
-      const uint64_t dk0 = desc_kmajor_sw128(smem_u32(sK)), dk1 = desc_kmajor_sw128(smem_u32(sK + C::kTileBytes));
+      // ring stage s = the stage-0 descriptor + s tiles in the start-address field (16-byte units)
+      const uint64_t dk0 = desc_kmajor_sw128(smem_u32(sK));
       const uint64_t dv0 = desc_mnmajor_sw128(smem_u32(sV), C::kBlockBytes);
-      const uint64_t dv1 = desc_mnmajor_sw128(smem_u32(sV + C::kTileBytes), C::kBlockBytes);
       while (true) {
         mbar_wait_warp(&bars.item_full[islot], iph);
         const int4 it = item_slot[islot];
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto tile_n = [&](int t) { return uint32_t(min(kGroupsPerTile, ng - t * kGroupsPerTile)) * 8u; };
         auto issue_s = [&](int t, int g, uint32_t kstage) {
           const uint32_t idesc = idesc_bf16_f32(128, tile_n(t), false);
-          const uint64_t kd = kstage ? dk1 : dk0, qd = (g && !split) ? dq1 : dq0;
+          const uint64_t kd = dk0 + uint64_t(kstage) * (C::kTileBytes >> 4), qd = (g && !split) ? dq1 : dq0;
           const uint32_t d = tmem + C::col_s(g);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
@@ -296,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         auto issue_pv = [&](int t, int g, uint32_t vstage, bool first) {
-          const uint64_t vd = vstage ? dv1 : dv0;
+          const uint64_t vd = dv0 + uint64_t(vstage) * (kVTile >> 4);
           const uint32_t ps = tmem + C::col_s(g), d = tmem + C::col_o(g);
           if (kFp8) {  // K = 32 keys per MMA: 8 TMEM columns of e4m3 P, 32 V rows (4 KB) of the stage
             const int ksteps = (int(tile_n(t)) + 31) / 32;
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
         auto next_k = [&] {
-          if (++ks == kStages) {
+          if (++ks == kSt) {
             ks = 0;
             kph ^= 1;
           }
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_commit_warp(&bars.o_full[g]);
             }
             mma_commit_warp(&bars.v_empty[vs]);
-            if (++vs == kStages) {
+            if (++vs == kSt) {
               vs = 0;
               vph ^= 1;
             }
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit_warp(&bars.k_empty[ks]);
         if (T == 1) mma_commit_warp(&bars.q_empty);
-        if (++ks == kStages) {
+        if (++ks == kSt) {
           ks = 0;
           kph ^= 1;
         }
@@ -406,11 +412,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit_warp(&bars.k_empty[ks]);
             if (t + 2 == T) mma_commit_warp(&bars.q_empty);
           }
-          if (++vs == kStages) {
+          if (++vs == kSt) {
             vs = 0;
             vph ^= 1;
           }
-          if (more && ++ks == kStages) {
+          if (more && ++ks == kSt) {
             ks = 0;
             kph ^= 1;
           }
@@ -719,13 +725,13 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
     const char* e = getenv("SVG2_EXP_POLY");
     return e ? atoi(e) : kDefaultPoly;
   }();
-  auto launch = [&](auto kernel) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes);
-    kernel<<<sms, kThreads, Cfg<D>::kSmemBytes, s>>>(mq, kv, p);
+  auto launch = [&](auto kernel, uint32_t smem = Cfg<D>::kSmemBytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kernel<<<sms, kThreads, smem, s>>>(mq, kv, p);
   };
   if constexpr (D == 128) {
     if (fp8) {
-      launch(k_varblock_attn<D, kDefaultPoly, true>);
+      launch(k_varblock_attn<D, kDefaultPoly, true>, Cfg<D>::kSmemBytesFp8);
       return cudaGetLastError();
     }
   }
