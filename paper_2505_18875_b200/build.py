@@ -1,4 +1,5 @@
 """Build libsvg2.so in-tree: hand-written CUDA for sm_100a only (nvcc cross-compiles without a GPU)."""
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -33,12 +34,17 @@ def build(force=False, verbose=False, out=None, defines=()):
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objdir = os.path.join(ROOT, "build", "obj" if out is None else "obj_variant")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    logs = []
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # one nvcc per translation unit, in parallel (the attention TUs dominate the build time)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, sources()))
+    objs = []
+    logs = []
+    for src, obj, r in results:
         logs.append(r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

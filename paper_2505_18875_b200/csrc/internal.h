@@ -120,9 +120,16 @@ struct KmeansInit {
   int role = 0;     // 0 = Q, 1 = K (part of the generator's stream id)
   int bh_base = 0;  // global (b,h) index of the first head of this launch (chunked calls keep the stream ids)
 };
+// Optional gather fused into the last update pass: Xp = pi X and Yp = pi Y (rows permuted by the final labels).
+struct KmeansGather {
+  void* Xp = nullptr;
+  const void* Y = nullptr;
+  void* Yp = nullptr;
+};
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
-                          cudaStream_t s, int* launches, const KmeansInit& init = KmeansInit());
+                          cudaStream_t s, int* launches, const KmeansInit& init = KmeansInit(),
+                          const KmeansGather& g = KmeansGather());
 cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH,
                                int Cq, int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
                                cudaStream_t s);

@@ -96,6 +96,15 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
   return SVG2_OK;
 }
 
+// A6 fused into the last k-means update (default), or separate gather launches (env SVG2_FUSE_GATHER=0, measurement)
+static bool fuse_gather_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SVG2_FUSE_GATHER");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 // The whole fused call for the heads of `dm` on stream s (arguments validated by the caller).  bh_base = global
 // (b,h) index of the first head (k-means++ stream ids of chunked calls, R25).
 cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_dims_t& dm, const svg2_config_t* cfg,
@@ -124,16 +133,29 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   init_q.role = 0;
   init_k.role = 1;
   init_q.bh_base = init_k.bh_base = bh_base;
+  // A6 rides on the last Lloyd update: that pass already reads every row through the final permutation, so it also
+  // writes Q' = pi_q Q, K' = pi_k K and (bf16 PV) V' = pi_k V
+  const bool fp8 = (cfg->flags & SVG2_FP8_PV) != 0;
+  const bool fuse_gather = fuse_gather_enabled();
+  KmeansGather gq, gk;
+  if (fuse_gather) {
+    gq.Xp = w.Qp;
+    gk.Xp = w.Kp;
+    if (!fp8) {
+      gk.Y = V;
+      gk.Yp = w.Vp;
+    }
+  }
   e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
-                    w.km, s, nullptr, init_q);
+                    w.km, s, nullptr, init_q, gq);
   mark(1);
   if (e == cudaSuccess)
     e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
-                      w.off_k, w.km, s, nullptr, init_k);
+                      w.off_k, w.km, s, nullptr, init_k, gk);
   mark(2);
-  if (e == cudaSuccess) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
-  const bool fp8 = (cfg->flags & SVG2_FP8_PV) != 0;
-  if (e == cudaSuccess) e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, fp8 ? nullptr : V, w.Vp, s);
+  if (e == cudaSuccess && !fuse_gather) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
+  if (e == cudaSuccess && !fuse_gather)
+    e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, fp8 ? nullptr : V, w.Vp, s);
   // FP8 PV (R26): V' in e4m3 with a per-head scale, written into the first half of the bf16 V' buffer
   if (e == cudaSuccess && fp8) e = launch_gather_rows_e4m3(w.perm_k, BH, dm.Nk, dm.d, V, w.Vp, w.v_amax, s);
   mark(3);
@@ -378,7 +400,9 @@ int32_t svg2_sparse_attention_launch_count(svg2_dims_t dm, const svg2_config_t* 
   (void)dm;
   if (!cfg) return 0;
   const bool warm = cfg->flags & SVG2_WARM_START;
-  int n = 2 * kmeans_launch_count(cfg->iters, warm) + 2 /*gathers*/ + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+  // the Q / K / V gathers are fused into the last k-means update (no launches of their own)
+  int n = 2 * kmeans_launch_count(cfg->iters, warm) + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+  if (!fuse_gather_enabled()) n += 2;
   if (cfg->flags & SVG2_FP8_PV) n += 2;  // |V| max per head + the e4m3 gather
   if (!warm && (cfg->flags & SVG2_INIT_KMEANSPP))
     n += kmeanspp_launch_count(dm.B * dm.H, dm.Nq, dm.d) + kmeanspp_launch_count(dm.B * dm.H, dm.Nk, dm.d) - 2;

@@ -212,13 +212,17 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
 // each warp keeps several row reads in flight (the loop is latency-bound otherwise).  Sums of bf16 values in fp64
 // are exact at these magnitudes, so the result does not depend on the order of the atomics: deterministic and
 // bit-identical to a sequential fp64 sum.
+// On the last iteration the same pass also writes the permuted copy X' = pi X (A6) and optionally Y' = pi Y (V,
+// which shares pi_k), so the fused call reads Q and K once less (no separate gather launches).
 constexpr int kSumRows = 64, kSumUnroll = 8, kSumWarps = 4;
 
-template <int D>
+template <int D, bool kGather>
 __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat16* __restrict__ X, int N, int C,
                                                              const int32_t* __restrict__ perm,
                                                              const int32_t* __restrict__ offsets,
-                                                             double* __restrict__ sum) {
+                                                             double* __restrict__ sum, __nv_bfloat16* __restrict__ Xp,
+                                                             const __nv_bfloat16* __restrict__ Y,
+                                                             __nv_bfloat16* __restrict__ Yp) {
   constexpr int kCols = D / 32;  // 4 (d = 128) or 2 (d = 64) bf16 per lane
   using Vec = typename std::conditional<kCols == 4, uint2, uint32_t>::type;
   const int bh = blockIdx.y, lane = threadIdx.x & 31;
@@ -233,6 +237,9 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
   }
   int j = lo, next = __ldg(off + j + 1);
   const Vec* Xv = reinterpret_cast<const Vec*>(X) + size_t(bh) * N * 32;  // 32 Vec per row
+  Vec* Xpv = kGather ? reinterpret_cast<Vec*>(Xp) + size_t(bh) * N * 32 : nullptr;
+  const Vec* Yv = kGather && Y ? reinterpret_cast<const Vec*>(Y) + size_t(bh) * N * 32 : nullptr;
+  Vec* Ypv = kGather && Yp ? reinterpret_cast<Vec*>(Yp) + size_t(bh) * N * 32 : nullptr;
   const int32_t* pm = perm + size_t(bh) * N;
   double* sb = sum + size_t(bh) * C * D;
   double acc[kCols];
@@ -255,6 +262,22 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
     for (int u = 0; u < kSumUnroll; ++u) {
       const int src = __shfl_sync(0xffffffffu, src_l, u);
       if (pb + u < p1) v[u] = __ldg(Xv + size_t(src) * 32 + lane);
+    }
+    if (kGather) {
+      if (Ypv) {  // the gather-only tensor (V' = pi_k V): loads in flight together with X's
+        Vec y[kSumUnroll];
+#pragma unroll
+        for (int u = 0; u < kSumUnroll; ++u) {
+          const int src = __shfl_sync(0xffffffffu, src_l, u);
+          if (pb + u < p1) y[u] = __ldg(Yv + size_t(src) * 32 + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < kSumUnroll; ++u)
+          if (pb + u < p1) Ypv[size_t(pb + u) * 32 + lane] = y[u];
+      }
+#pragma unroll
+      for (int u = 0; u < kSumUnroll; ++u)
+        if (pb + u < p1) Xpv[size_t(pb + u) * 32 + lane] = v[u];
     }
 #pragma unroll
     for (int u = 0; u < kSumUnroll; ++u) {
@@ -300,7 +323,8 @@ __global__ void k_init_cold(const __nv_bfloat16* __restrict__ X, int N, int C, f
 template <int D>
 cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, const KmeansInit& init,
                        float* cent, int32_t* labels,
-                       int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws, cudaStream_t s) {
+                       int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws, cudaStream_t s,
+                       const KmeansGather& g) {
   const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(Xv);
   const int Cpad = cent_pad(C);
   CUtensorMap mx, mh, ml;
@@ -327,8 +351,15 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
     k_assign_tc<D><<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
-    k_update_sum<D><<<dim3((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH), 32 * kSumWarps, 0, s>>>(
-        X, N, C, perm, offsets, ws.c_sum);
+    const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
+    if (it + 1 == iters && g.Xp)
+      k_update_sum<D, true><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, ws.c_sum,
+                                                                 static_cast<__nv_bfloat16*>(g.Xp),
+                                                                 static_cast<const __nv_bfloat16*>(g.Y),
+                                                                 static_cast<__nv_bfloat16*>(g.Yp));
+    else
+      k_update_sum<D, false><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, ws.c_sum, nullptr, nullptr,
+                                                                  nullptr);
     k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, offsets, ws.c_sum, cent);
   }
   return cudaGetLastError();
@@ -341,7 +372,7 @@ int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * 
 
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
-                          cudaStream_t s, int* launches, const KmeansInit& init) {
+                          cudaStream_t s, int* launches, const KmeansInit& init, const KmeansGather& g) {
   if (!perm) perm = ws.perm;
   if (!offsets) offsets = ws.offsets;
   if (launches) {
@@ -349,8 +380,8 @@ cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters,
     if (!warm && init.kmeanspp) *launches += kmeanspp_launch_count(BH, N, d) - 1;  // replaces the strided init
   }
   if (d == 128)
-    return run_kmeans<128>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s);
-  return run_kmeans<64>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s);
+    return run_kmeans<128>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s, g);
+  return run_kmeans<64>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s, g);
 }
 
 }  // namespace svg2

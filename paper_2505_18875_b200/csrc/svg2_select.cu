@@ -6,19 +6,23 @@
 // The order of every floating-point operation is fixed by the specification above (not by shared code with the
 // oracle), so the mask is bit-exact against it except at documented near-ties (R17).
 #include <cfloat>
-#include <climits>
 #include "internal.h"
 
 namespace svg2 {
 namespace {
 
 constexpr int kSelThreads = 256;
-constexpr int kKChunk = 32;  // centroid columns staged per pass (rows padded to kKChunk + 1 floats)
+constexpr int kEq1Unroll = 8;  // 16-byte key-centroid loads in flight per thread (the Eq. 1 loop is L2-latency-bound)
 
 __device__ __forceinline__ bool before(double wa, int ja, double wb, int jb) {
   return wa > wb || (wa == wb && ja < jb);
 }
 
+// One CTA per (query cluster i, bh).  Eq. 1 per key cluster j by one thread: its sequential FMA chain over k, the key
+// centroid row read straight from L2 with kEq1Unroll 16-byte loads in flight (no staging barriers), the query
+// centroid broadcast from shared memory.  Eq. 2 weights, Z_i summed by one thread in ascending j with its loads
+// issued ahead of the dependent adds, a shared-memory bitonic sort (w desc, j asc), and the top-p walk (R11) by one
+// thread over prefetched chunks of the sorted order.
 __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict__ cq, const float* __restrict__ ck,
                                                         const int32_t* __restrict__ sq, const int32_t* __restrict__ sk,
                                                         int Cq, int Ck, int d, double scale, double top_p, int sortN,
@@ -28,14 +32,14 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
   double* w = reinterpret_cast<double*>(smem);          // [sortN]
   double* crow = w + sortN;                             // [d]
   int* idx = reinterpret_cast<int*>(crow + d);          // [sortN]
-  int* sks = idx + sortN;                                  // [Ck] key-cluster sizes (staged for the serial walk)
-  uint8_t* sel = reinterpret_cast<uint8_t*>(sks + Ck);     // [Ck]
-  float* stage = reinterpret_cast<float*>(sks + Ck + (Ck + 3) / 4 + 4);  // [kSelThreads][kKChunk + 1]
+  int* sks = idx + sortN;                               // [Ck] key-cluster sizes
+  uint8_t* sel = reinterpret_cast<uint8_t*>(sks + Ck);  // [Ck]
   __shared__ double red[kSelThreads / 32];
+  __shared__ double Z_sh;
   __shared__ long long keys_sh;
-  const int i = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
+  const int i = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const float* cqi = cq + (size_t(bh) * Cq + i) * d;
-  const float* ckb = ck + size_t(bh) * Ck * d;
+  const float4* ckb = reinterpret_cast<const float4*>(ck + size_t(bh) * Ck * d);
   const int32_t* skb = sk + size_t(bh) * Ck;
   for (int k = tid; k < d; k += kSelThreads) crow[k] = double(cqi[k]);
   for (int j = tid; j < Ck; j += kSelThreads) {
@@ -43,63 +47,70 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
     sks[j] = __ldg(skb + j);
   }
   __syncthreads();
-  // Eq. 1: the key centroids are staged kSelThreads rows x kKChunk columns at a time through padded shared memory
-  // (coalesced global reads, conflict-free row reads); each thread keeps its own sequential FMA chain over k.
+  // Eq. 1: S_ij = scale * (sequential fp64 FMA over k ascending)
   double m = -INFINITY;
-  for (int j0 = 0; j0 < Ck; j0 += kSelThreads) {
-    const int j = j0 + tid;
+  for (int j = tid; j < Ck; j += kSelThreads) {
+    const float4* row = ckb + size_t(j) * (d / 4);
     double acc = 0.0;
-    for (int k0 = 0; k0 < d; k0 += kKChunk) {
-      __syncthreads();
-      for (int e = tid; e < kSelThreads * kKChunk; e += kSelThreads) {
-        const int r = e / kKChunk, c = e - r * kKChunk;
-        stage[r * (kKChunk + 1) + c] = (j0 + r < Ck) ? __ldg(ckb + size_t(j0 + r) * d + k0 + c) : 0.f;
+    for (int k4 = 0; k4 < d / 4; k4 += kEq1Unroll) {
+      float4 c[kEq1Unroll];
+#pragma unroll
+      for (int u = 0; u < kEq1Unroll; ++u) c[u] = __ldg(row + k4 + u);
+#pragma unroll
+      for (int u = 0; u < kEq1Unroll; ++u) {
+        const double* q = crow + 4 * (k4 + u);
+        acc = fma(q[0], double(c[u].x), acc);
+        acc = fma(q[1], double(c[u].y), acc);
+        acc = fma(q[2], double(c[u].z), acc);
+        acc = fma(q[3], double(c[u].w), acc);
       }
-      __syncthreads();
-      const float* srow = stage + tid * (kKChunk + 1);
-#pragma unroll 8
-      for (int k = 0; k < kKChunk; ++k) acc = fma(crow[k0 + k], double(srow[k]), acc);
     }
-    if (j < Ck) {
-      const double S = scale * acc;
-      w[j] = S;
-      if (sks[j] > 0) m = fmax(m, S);
-    }
+    const double S = scale * acc;
+    w[j] = S;
+    if (sks[j] > 0) m = fmax(m, S);
   }
-  // block max (exact, order-free)
+  // block max over non-empty clusters (exact, order-free)
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((tid & 31) == 0) red[tid >> 5] = m;
+  if (lane == 0) red[tid >> 5] = m;
   __syncthreads();
   m = red[0];
   for (int t = 1; t < kSelThreads / 32; ++t) m = fmax(m, red[t]);
+  // Eq. 2: w_ij = |K_j| exp(S_ij - m_i); empty clusters weigh 0; sort padding sorts last
   for (int j = tid; j < sortN; j += kSelThreads) {
     if (j < Ck) {
-      const int s = __ldg(skb + j);
+      const int s = sks[j];
       w[j] = s > 0 ? double(s) * exp(w[j] - m) : 0.0;
       idx[j] = j;
     } else {
       w[j] = -1.0;
-      idx[j] = INT_MAX;
+      idx[j] = 0x7fffffff;
     }
   }
   __syncthreads();
-  if (top_p >= 1.0) {
+  if (top_p >= 1.0) {  // p = 1: exactly the non-empty clusters (R11), no order needed
     long long keys = 0;
     for (int j = tid; j < Ck; j += kSelThreads) {
-      const int s = __ldg(skb + j);
+      const int s = sks[j];
       sel[j] = s > 0;
       keys += s;
     }
     for (int o = 16; o > 0; o >>= 1) keys += __shfl_xor_sync(0xffffffffu, keys, o);
     if (tid == 0) keys_sh = 0;
     __syncthreads();
-    if ((tid & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&keys_sh), (unsigned long long)keys);
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&keys_sh), (unsigned long long)keys);
     __syncthreads();
   } else {
-    __shared__ double Z_sh;
-    if (tid == 0) {  // Z_i in ascending j, sequential (spec order)
+    if (tid == 0) {  // Z_i in ascending j, sequential (spec order); the loads run ahead of the dependent adds
       double Z = 0.0;
-      for (int j = 0; j < Ck; ++j) Z = Z + w[j];
+      int j = 0;
+      for (; j + 8 <= Ck; j += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = w[j + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) Z = Z + v[u];
+      }
+      for (; j < Ck; ++j) Z = Z + w[j];
       Z_sh = Z;
     }
     // bitonic sort of (w desc, j asc) over sortN (power of two >= Ck)
@@ -124,17 +135,31 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
       }
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {  // the top-p walk in sorted order (R11): take rank r while the mass before it is < p Z_i
       const double target = top_p * Z_sh;
       double cum = 0.0;
       long long keys = 0;
-      for (int r = 0; r < Ck; ++r) {
-        const double wr = w[r];
-        if (wr <= 0.0) break;
-        if (!(cum < target)) break;
-        sel[idx[r]] = 1;
-        keys += sks[idx[r]];
-        cum = cum + wr;
+      bool done = false;
+      for (int r0 = 0; r0 < Ck && !done; r0 += 8) {
+        double wr[8];
+        int jr[8], sr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // sortN >= r0 + 8 whenever Ck > r0 (sortN is a power of two >= 8 here)
+          wr[u] = w[r0 + u];
+          jr[u] = idx[r0 + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sr[u] = (r0 + u < Ck) ? sks[jr[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (done || r0 + u >= Ck || wr[u] <= 0.0 || !(cum < target)) {
+            done = true;
+          } else {
+            sel[jr[u]] = 1;
+            keys += sr[u];
+            cum = cum + wr[u];
+          }
+        }
       }
       keys_sh = keys;
     }
@@ -153,11 +178,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
 cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH, int Cq,
                                int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
                                cudaStream_t s) {
-  int sortN = 1;
+  int sortN = 8;
   while (sortN < Ck) sortN <<= 1;
   const size_t smem = size_t(sortN) * sizeof(double) + size_t(d) * sizeof(double) + size_t(sortN) * sizeof(int) +
-                      size_t(Ck) * sizeof(int) + (size_t(Ck) / 4 + 5) * sizeof(int) +
-                      size_t(kSelThreads) * (kKChunk + 1) * sizeof(float);
+                      size_t(Ck) * sizeof(int) + size_t(Ck);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
