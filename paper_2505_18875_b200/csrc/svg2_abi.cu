@@ -49,7 +49,7 @@ struct FusedWs {
   void *Qp, *Kp, *Vp;
   uint8_t* mask;
   uint32_t* v_amax;  // FP8 PV: per-head max |V| (f32 bits)
-  KmeansWs km;
+  KmeansWs km_q, km_k;  // per-role k-means scratch: the two roles may run concurrently
   AttnWs attn;
 };
 
@@ -69,14 +69,8 @@ FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) 
   w.Vp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.mask = c.take<uint8_t>(BH * cfg.Cq * cfg.Ck);
   w.v_amax = c.take<uint32_t>(BH);
-  // k-means scratch is reused by the Q and the K role (same stream, sequential): carve the larger one
-  Carver probe_q(nullptr), probe_k(nullptr);
-  carve_kmeans(probe_q, int(BH), dm.Nq, cfg.Cq);
-  carve_kmeans(probe_k, int(BH), dm.Nk, cfg.Ck);
-  const size_t start = (c.off + 255) & ~size_t(255);
-  Carver km(c.base ? c.base + start : nullptr);
-  w.km = probe_q.off >= probe_k.off ? carve_kmeans(km, int(BH), dm.Nq, cfg.Cq) : carve_kmeans(km, int(BH), dm.Nk, cfg.Ck);
-  c.off = start + km.off;
+  w.km_q = carve_kmeans(c, int(BH), dm.Nq, cfg.Cq);
+  w.km_k = carve_kmeans(c, int(BH), dm.Nk, cfg.Ck);
   w.attn = carve_attn(c, int(BH), dm.Nq, dm.Nk, cfg.Cq, cfg.Ck);
   return w;
 }
@@ -100,6 +94,16 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
 static bool fuse_gather_enabled() {
   static const bool on = [] {
     const char* e = getenv("SVG2_FUSE_GATHER");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+// The Q and K k-means run on two streams (fork / join through events; env SVG2_ROLE_STREAMS=0: one stream) so the
+// latency-bound kernels of one role overlap the other role's
+static bool role_streams_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SVG2_ROLE_STREAMS");
     return !e || atoi(e) != 0;
   }();
   return on;
@@ -146,12 +150,32 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
       gk.Yp = w.Vp;
     }
   }
+  // Q role on a forked stream, K role on s; the k-means++ cold start (cooperative launches) stays on one stream
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (role_streams_enabled() && !(!warm && init_q.kmeanspp)) {
+    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(s2, ev_fork, 0) != cudaSuccess) {
+      if (s2) cudaStreamDestroy(s2);
+      s2 = nullptr;
+      (void)cudaGetLastError();
+    }
+  }
   e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
-                    w.km, s, nullptr, init_q, gq);
-  mark(1);
+                    w.km_q, s2 ? s2 : s, nullptr, init_q, gq);
+  mark(1);  // with two streams: the fork point (stage "kmeans_k" then covers both roles)
   if (e == cudaSuccess)
     e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
-                      w.off_k, w.km, s, nullptr, init_k, gk);
+                      w.off_k, w.km_k, s, nullptr, init_k, gk);
+  if (s2) {  // join (always, so no work is left behind on s2 even after an error) and release (deferred by CUDA)
+    cudaEventRecord(ev_join, s2);
+    cudaStreamWaitEvent(s, ev_join, 0);
+    cudaStreamDestroy(s2);
+  }
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   mark(2);
   if (e == cudaSuccess && !fuse_gather) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
   if (e == cudaSuccess && !fuse_gather)

@@ -343,9 +343,9 @@ def test_abi_errors(svg2):
 
 
 # ------------------------------------------------------------------ full size, bench launch configuration
-@pytest.mark.parametrize("name", ["hunyuan720p"])
+@pytest.mark.parametrize("name", ["hunyuan720p", "wan720p"])
 def test_fullsize_sampled_rows(svg2, oracle_mod, name):
-    """BASELINE configs[1] at full size through the fused call (cold 5 iterations, then a warm 2-iteration call as
+    """BASELINE configs[1] and [2] at full size through the fused call (cold 5 iterations, then a warm 2-iteration call as
     bench.py times it); the oracle checks sampled query rows of two heads, fed with the GPU's intermediates."""
     wl = svg2_synth.WORKLOADS[name]
     q, k, v = svg2_synth.generate(wl)
