@@ -153,7 +153,9 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   // Q role on a forked stream, K role on s; the k-means++ cold start (cooperative launches) stays on one stream
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (role_streams_enabled() && !(!warm && init_q.kmeanspp)) {
+  cudaStreamCaptureStatus capture = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &capture);  // inside a graph capture: stay on the caller's stream (no stream creation)
+  if (role_streams_enabled() && !(!warm && init_q.kmeanspp) && capture == cudaStreamCaptureStatusNone) {
     if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||

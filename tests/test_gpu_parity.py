@@ -309,6 +309,32 @@ def test_deterministic(svg2):
     assert torch.equal(O1, O2) and torch.equal(p1, p2) and torch.equal(e1["k_centroids"], e2["k_centroids"])
 
 
+def test_cuda_graph_capture_replay(svg2):
+    """The fused warm call captured into a CUDA graph (inside a capture the library stays on the capture stream) and
+    replayed on new inputs gives bitwise the eager call's output on those inputs."""
+    Q, K, V, Cq, Ck, p, iters = _pipeline_inputs(svg2, (1, 2, 3000, 3000, 128, 40, 80), seed=11)
+    _, _, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, iters, p)
+    cq0, ck0 = ex["q_centroids"].clone(), ex["k_centroids"].clone()
+    Qs, Ks, Vs = Q.clone(), K.clone(), V.clone()
+    cq, ck = cq0.clone(), ck0.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up on the capture stream (workspace allocated outside the capture)
+        svg2.sparse_attention(Qs, Ks, Vs, Cq, Ck, 2, p, cq, ck, warm=True)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        O_g, pairs_g, _ = svg2.sparse_attention(Qs, Ks, Vs, Cq, Ck, 2, p, cq, ck, warm=True)
+    Q2, K2, V2, *_ = _pipeline_inputs(svg2, (1, 2, 3000, 3000, 128, 40, 80), seed=12)
+    Qs.copy_(Q2), Ks.copy_(K2), Vs.copy_(V2), cq.copy_(cq0), ck.copy_(ck0)
+    g.replay()
+    torch.cuda.synchronize()
+    O_e, pairs_e, _ = svg2.sparse_attention(Q2, K2, V2, Cq, Ck, 2, p, cq0.clone(), ck0.clone(), warm=True)
+    torch.cuda.synchronize()
+    assert torch.equal(O_g, O_e) and torch.equal(pairs_g, pairs_e)
+
+
 def test_warm_start_cache(svg2):
     q, k, v = random_qkv(1, 2, 3000, 3000, 128, seed=4)
     Q, K, V = to_dev(q), to_dev(k), to_dev(v)
