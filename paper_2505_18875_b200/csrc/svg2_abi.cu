@@ -12,7 +12,7 @@ namespace {
 
 constexpr long long kMaxN = 1ll << 24;
 constexpr int kMaxHostChunks = 64;
-constexpr int kHostChunks = 6;  // middle chunks of the host pipeline (e2e, HunyuanVideo: 67.1 / 63.4 / 63.1 / 61.7 ms with 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; env SVG2_HOST_CHUNKS / SVG2_HOST_RAMP override)
+constexpr int kHostChunks = 6;  // middle chunks of the host pipeline (e2e, HunyuanVideo, one compute stream: 67.1 / 63.4 / 63.1 / 61.7 ms with 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; two compute streams: 59.7 / 57.5 / 58.4 ms with 4 / 6 / 9; env SVG2_HOST_CHUNKS / SVG2_HOST_RAMP override)
 
 svg2_status_t check_device() {
   int dev = 0, major = 0, minor = 0;
@@ -251,7 +251,7 @@ HostPlan host_plan(const svg2_dims_t& dm) {
 }
 struct HostWs {
   void *Q[2], *K[2], *V[2], *O[2];
-  FusedWs fused;
+  FusedWs fused[2];  // one per compute stream: consecutive chunks run concurrently
 };
 HostWs carve_host(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg, const HostPlan& p) {
   HostWs w;
@@ -263,7 +263,8 @@ HostWs carve_host(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg, co
     w.O[i] = c.take<uint16_t>(q);
   }
   const svg2_dims_t chunk{1, p.hc, dm.Nq, dm.Nk, dm.d};
-  w.fused = carve_fused(c, chunk, cfg);
+  w.fused[0] = carve_fused(c, chunk, cfg);
+  w.fused[1] = carve_fused(c, chunk, cfg);
   return w;
 }
 }  // namespace
@@ -471,11 +472,20 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   Carver c(ws);
   HostWs w = carve_host(c, dm, *cfg, plan);
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
-  // three internal streams: copies in, compute, copies out; events order them per chunk and slot
-  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  // four internal streams: copies in, two compute streams (chunk parity: the next chunk's k-means, selection and first
+  // attention items fill the SMs the current chunk's attention tail leaves idle), copies out; events order them per
+  // chunk and slot.  The k-means++ cold start (cooperative launches) keeps one compute stream.
+  static const int compute_streams_env = [] {
+    const char* v = getenv("SVG2_HOST_COMPUTE_STREAMS");
+    return v ? atoi(v) : 2;
+  }();
+  const bool pp_cold = !(cfg->flags & SVG2_WARM_START) && (cfg->flags & SVG2_INIT_KMEANSPP);
+  const int ncomp = (compute_streams_env >= 2 && !pp_cold) ? 2 : 1;
+  cudaStream_t sin = nullptr, scomp[2] = {nullptr, nullptr}, sout = nullptr;
   cudaEvent_t start = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&scomp[0], cudaStreamNonBlocking);
+  if (e == cudaSuccess && ncomp == 2) e = cudaStreamCreateWithFlags(&scomp[1], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
   const int n = plan.nchunks;
@@ -483,11 +493,12 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   for (int i = 0; e == cudaSuccess && i < 3 * n; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(start, caller);  // after the caller's earlier work
   if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, start, 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(scomp, start, 0);
+  for (int i = 0; i < ncomp && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(scomp[i], start, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, start, 0);
   const size_t qrow = size_t(dm.Nq) * dm.d * 2, krow = size_t(dm.Nk) * dm.d * 2;  // bytes per head
   for (int ci = 0; e == cudaSuccess && ci < n; ++ci) {
     const int bh0 = plan.start[ci], nh = plan.start[ci + 1] - bh0, slot = ci & 1;
+    cudaStream_t sc = scomp[ncomp == 2 ? slot : 0];
     cudaEvent_t in = ev[3 * ci], done = ev[3 * ci + 1], out = ev[3 * ci + 2];
     if (ci >= 2) e = cudaStreamWaitEvent(sin, ev[3 * (ci - 2) + 1], 0);  // slot's inputs consumed
     if (e == cudaSuccess)
@@ -497,28 +508,32 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.V[slot], static_cast<const uint8_t*>(Vh) + bh0 * krow, nh * krow, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaEventRecord(in, sin);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(scomp, in, 0);
-    if (e == cudaSuccess && ci >= 2) e = cudaStreamWaitEvent(scomp, ev[3 * (ci - 2) + 2], 0);  // slot's output read
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, in, 0);
+    if (e == cudaSuccess && ci >= 2) e = cudaStreamWaitEvent(sc, ev[3 * (ci - 2) + 2], 0);  // slot's output read
     if (e == cudaSuccess) {
       const svg2_dims_t cd{1, nh, dm.Nq, dm.Nk, dm.d};
       e = run_fused(w.Q[slot], w.K[slot], w.V[slot], cd, cfg, q_centroids + size_t(bh0) * cfg->Cq * dm.d,
                     k_centroids + size_t(bh0) * cfg->Ck * dm.d, w.O[slot],
-                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused, scomp, bh0);
+                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused[ncomp == 2 ? slot : 0], sc, bh0);
     }
-    if (e == cudaSuccess) e = cudaEventRecord(done, scomp);
+    if (e == cudaSuccess) e = cudaEventRecord(done, sc);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, done, 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(static_cast<uint8_t*>(Oh) + bh0 * qrow, w.O[slot], nh * qrow, cudaMemcpyDeviceToHost, sout);
     if (e == cudaSuccess) e = cudaEventRecord(out, sout);
   }
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 2], 0);  // the last copy out ends the call
+  // the last copy out ends the call (sout is in order and each copy waited for its chunk); the last two chunks'
+  // compute events as well, so no work of either compute stream outlives the call
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 2], 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 1], 0);
+  if (e == cudaSuccess && n >= 2) e = cudaStreamWaitEvent(caller, ev[3 * (n - 2) + 1], 0);
   for (int i = 0; i < 3 * n; ++i)
     if (ev[i]) cudaEventDestroy(ev[i]);
   delete[] ev;
   if (start) cudaEventDestroy(start);
   if (sin) cudaStreamDestroy(sin);  // released once their queued work completes
-  if (scomp) cudaStreamDestroy(scomp);
+  for (int i = 0; i < 2; ++i)
+    if (scomp[i]) cudaStreamDestroy(scomp[i]);
   if (sout) cudaStreamDestroy(sout);
   return from_cuda(e);
 }
