@@ -125,6 +125,7 @@ struct KmeansGather {
   void* Xp = nullptr;
   const void* Y = nullptr;
   void* Yp = nullptr;
+  cudaEvent_t wait_y = nullptr;  // Y may still be arriving (host pipeline): the gather pass waits for this event
 };
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,

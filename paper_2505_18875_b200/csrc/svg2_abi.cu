@@ -113,7 +113,10 @@ static bool role_streams_enabled() {
 // (b,h) index of the first head (k-means++ stream ids of chunked calls, R25).
 cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_dims_t& dm, const svg2_config_t* cfg,
                       float* q_centroids, float* k_centroids, void* O, int64_t* selected_pairs,
-                      const svg2_debug_t* dbg, FusedWs w, cudaStream_t s, int bh_base) {
+                      const svg2_debug_t* dbg, FusedWs w, cudaStream_t s, int bh_base,
+                      const cudaEvent_t* arrive = nullptr) {
+  // arrive (host pipeline): events of Q, K and V landing in device memory; each role waits only for its own tensor,
+  // V only before the pass that gathers it
   if (dbg) {  // intermediates requested: write them straight into the caller's buffers
     if (dbg->q_labels) w.lab_q = dbg->q_labels;
     if (dbg->k_labels) w.lab_k = dbg->k_labels;
@@ -165,9 +168,14 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
       (void)cudaGetLastError();
     }
   }
+  if (arrive) {
+    cudaStreamWaitEvent(s2 ? s2 : s, arrive[0], 0);
+    if (gk.Yp) gk.wait_y = arrive[2];
+  }
   e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
                     w.km_q, s2 ? s2 : s, nullptr, init_q, gq);
   mark(1);  // with two streams: the fork point (stage "kmeans_k" then covers both roles)
+  if (arrive) cudaStreamWaitEvent(s, arrive[1], 0);
   if (e == cudaSuccess)
     e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
                       w.off_k, w.km_k, s, nullptr, init_k, gk);
@@ -179,6 +187,7 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   mark(2);
+  if (arrive && !gk.wait_y) cudaStreamWaitEvent(s, arrive[2], 0);  // V gathered by a separate pass
   if (e == cudaSuccess && !fuse_gather) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
   if (e == cudaSuccess && !fuse_gather)
     e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, fp8 ? nullptr : V, w.Vp, s);
@@ -489,8 +498,10 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
   const int n = plan.nchunks;
-  cudaEvent_t* ev = new cudaEvent_t[3 * n]();  // per chunk: inputs in, computed, output out
+  cudaEvent_t* ev = new cudaEvent_t[3 * n]();  // per chunk: inputs in (V, the last copy), computed, output out
+  cudaEvent_t* evqk = new cudaEvent_t[2 * n]();  // per chunk: Q in, K in
   for (int i = 0; e == cudaSuccess && i < 3 * n; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  for (int i = 0; e == cudaSuccess && i < 2 * n; ++i) e = cudaEventCreateWithFlags(&evqk[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(start, caller);  // after the caller's earlier work
   if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, start, 0);
   for (int i = 0; i < ncomp && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(scomp[i], start, 0);
@@ -503,18 +514,21 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
     if (ci >= 2) e = cudaStreamWaitEvent(sin, ev[3 * (ci - 2) + 1], 0);  // slot's inputs consumed
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.Q[slot], static_cast<const uint8_t*>(Qh) + bh0 * qrow, nh * qrow, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaEventRecord(evqk[2 * ci], sin);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.K[slot], static_cast<const uint8_t*>(Kh) + bh0 * krow, nh * krow, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaEventRecord(evqk[2 * ci + 1], sin);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.V[slot], static_cast<const uint8_t*>(Vh) + bh0 * krow, nh * krow, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaEventRecord(in, sin);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, in, 0);
     if (e == cudaSuccess && ci >= 2) e = cudaStreamWaitEvent(sc, ev[3 * (ci - 2) + 2], 0);  // slot's output read
     if (e == cudaSuccess) {
       const svg2_dims_t cd{1, nh, dm.Nq, dm.Nk, dm.d};
+      const cudaEvent_t arrive[3] = {evqk[2 * ci], evqk[2 * ci + 1], in};  // the computation starts on Q alone
       e = run_fused(w.Q[slot], w.K[slot], w.V[slot], cd, cfg, q_centroids + size_t(bh0) * cfg->Cq * dm.d,
                     k_centroids + size_t(bh0) * cfg->Ck * dm.d, w.O[slot],
-                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused[ncomp == 2 ? slot : 0], sc, bh0);
+                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused[ncomp == 2 ? slot : 0], sc, bh0,
+                    arrive);
     }
     if (e == cudaSuccess) e = cudaEventRecord(done, sc);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, done, 0);
@@ -529,7 +543,10 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   if (e == cudaSuccess && n >= 2) e = cudaStreamWaitEvent(caller, ev[3 * (n - 2) + 1], 0);
   for (int i = 0; i < 3 * n; ++i)
     if (ev[i]) cudaEventDestroy(ev[i]);
+  for (int i = 0; i < 2 * n; ++i)
+    if (evqk[i]) cudaEventDestroy(evqk[i]);
   delete[] ev;
+  delete[] evqk;
   if (start) cudaEventDestroy(start);
   if (sin) cudaStreamDestroy(sin);  // released once their queued work completes
   for (int i = 0; i < 2; ++i)

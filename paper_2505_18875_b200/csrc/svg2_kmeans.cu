@@ -471,6 +471,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
     const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
     // the gather pass (last iteration) uses the asynchronous-copy kernel: K' + V' 0.69 -> 0.48 ms, Q' equal; the
     // plain update keeps the register-staged one (0.20 ms vs 0.33 ms: its accumulation phase has no loads in flight)
+    if (it + 1 == iters && g.wait_y) cudaStreamWaitEvent(s, g.wait_y, 0);
     if (update_async() && it + 1 == iters && g.Xp) {
       constexpr int rows = kAsyncRows<true>;
       const dim3 grid_a((N + rows * kAsyncWarps - 1) / (rows * kAsyncWarps), BH);
