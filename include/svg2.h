@@ -157,7 +157,10 @@ SVG2_API svg2_status_t svg2_unpermute(const void* Op, const int32_t* perm, int32
  * k-means(Q; Cq) and k-means(K; Ck) with the centroid cache (q_centroids [B,H,Cq,d], k_centroids [B,H,Ck,d]
  * f32, read iff config->flags & SVG2_WARM_START, always written back), permutation, selection, variable-block
  * attention with the unpermute fused into its epilogue.  O [B,H,Nq,d] bf16 out in original token order.
- * selected_pairs [B,H] int64 out (nullable).  dbg: NULL or intermediates / stage events (see svg2_debug_t). */
+ * selected_pairs [B,H] int64 out (nullable).  dbg: NULL or intermediates / stage events (see svg2_debug_t).
+ * Streams: the Q-role k-means runs on a stream forked from `stream` for the duration of the call (event fork /
+ * join, created and released per call; not while `stream` is being captured into a CUDA graph, where the call
+ * stays on `stream` and is capture-safe); all work is ordered after, and joined back into, `stream`. */
 SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V, svg2_dims_t dims,
                                     const svg2_config_t* config, float* q_centroids, float* k_centroids, void* O,
                                     int64_t* selected_pairs, const svg2_debug_t* dbg, void* ws, size_t ws_bytes,
@@ -167,8 +170,10 @@ SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const
  * in host memory (page-locked for the copies to overlap; pageable memory works but serialises).  Same math and
  * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (small first and last ones,
  * then 6 equal middle ones): the copy of
- * chunk c+1 to the device and of chunk c-1 back to the host overlap the computation of chunk c (internal streams,
- * double-buffered device staging in the workspace, SVG2_ENTRY_SPARSE_ATTENTION_HOST).  The centroid caches and
+ * chunk c+1 to the device and of chunk c-1 back to the host overlap the computation of chunk c, consecutive chunks
+ * compute on two alternating streams, and each role of a chunk waits only for its own tensor's upload (internal
+ * streams, double-buffered device staging and two fused-call workspaces in the workspace,
+ * SVG2_ENTRY_SPARSE_ATTENTION_HOST).  The centroid caches and
  * selected_pairs are DEVICE buffers as in svg2_sparse_attention.  The work is ordered after the work already queued
  * on `stream`, and later work on `stream` waits for it; Oh is complete when `stream` has synchronised. */
 SVG2_API svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const void* Vh, svg2_dims_t dims,
