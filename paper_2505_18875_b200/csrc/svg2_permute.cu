@@ -62,39 +62,54 @@ __device__ int block_exclusive_scan(int v, int* total) {
 }
 
 constexpr int kScanThreads = 1024;
-constexpr int kBinsPerThread = kMaxClusters / kScanThreads;  // 4
 
+// One CTA per (b,h).  Bin j = b * kScanThreads + threadIdx.x (consecutive threads own consecutive clusters, so all
+// threads work for any C); the loops over the T tiles keep 8 loads in flight.  Round b scans its kScanThreads bins
+// and carries the running total into round b + 1.
 __global__ void __launch_bounds__(kScanThreads) k_scan(int N, int C, int T, int32_t* __restrict__ counts,
                                                        int32_t* __restrict__ offsets, int32_t* __restrict__ sizes) {
   const int bh = blockIdx.x;
   int32_t* cnt = counts + size_t(bh) * T * C;
-  int tot[kBinsPerThread];
-  int local = 0;
+  int carry = 0;
+  for (int b = 0; b * kScanThreads < C; ++b) {
+    const int bin = b * kScanThreads + threadIdx.x;
+    int tot = 0;
+    if (bin < C) {
+      int t = 0;
+      for (; t + 8 <= T; t += 8) {
+        int v[8];
 #pragma unroll
-  for (int b = 0; b < kBinsPerThread; ++b) {
-    const int bin = threadIdx.x * kBinsPerThread + b;
-    int s = 0;
-    if (bin < C)
-      for (int t = 0; t < T; ++t) s += cnt[size_t(t) * C + bin];
-    tot[b] = s;
-    local += s;
-  }
-  int total;
-  int run = block_exclusive_scan<kScanThreads>(local, &total);
+        for (int u = 0; u < 8; ++u) v[u] = cnt[size_t(t + u) * C + bin];
 #pragma unroll
-  for (int b = 0; b < kBinsPerThread; ++b) {
-    const int bin = threadIdx.x * kBinsPerThread + b;
+        for (int u = 0; u < 8; ++u) tot += v[u];
+      }
+      for (; t < T; ++t) tot += cnt[size_t(t) * C + bin];
+    }
+    int total;
+    const int run = carry + block_exclusive_scan<kScanThreads>(tot, &total);
     if (bin < C) {
       offsets[size_t(bh) * (C + 1) + bin] = run;
-      if (sizes) sizes[size_t(bh) * C + bin] = tot[b];
+      if (sizes) sizes[size_t(bh) * C + bin] = tot;
       int base = run;
-      for (int t = 0; t < T; ++t) {
+      int t = 0;
+      for (; t + 8 <= T; t += 8) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = cnt[size_t(t + u) * C + bin];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          cnt[size_t(t + u) * C + bin] = base;  // becomes the first output position of (tile t + u, cluster bin)
+          base += v[u];
+        }
+      }
+      for (; t < T; ++t) {
         const int c = cnt[size_t(t) * C + bin];
-        cnt[size_t(t) * C + bin] = base;  // becomes the first output position of (tile t, cluster bin)
+        cnt[size_t(t) * C + bin] = base;
         base += c;
       }
     }
-    run += tot[b];
+    carry += total;
+    __syncthreads();  // block_exclusive_scan's shared scratch is reused by the next round
   }
   if (threadIdx.x == 0) offsets[size_t(bh) * (C + 1) + C] = N;
 }
