@@ -633,23 +633,34 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   __syncthreads();
   const int rowbase = int(size_t(bh) * Nk);
   int2* grp = ws.groups + li * ws.gcap;
-  auto group_at = [&](int gi) -> int2 {
-    if (gi >= ng_real) return make_int2(rowbase + run_s[0], 0);  // the padding group: valid rows, all masked
-    int lo = 0, hi = nrun - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (run_g[mid] <= gi) lo = mid; else hi = mid - 1;
-    }
-    const int row = run_s[lo] + 8 * (gi - run_g[lo]);
-    return make_int2(rowbase + row, min(8, run_e[lo] - row));
-  };
-  for (int gi = tid; gi < ng; gi += kBuildThreads) grp[gi] = group_at(gi);
+  // one thread per 16-group tile: locate the tile's first group by binary search, then walk the runs forward,
+  // writing the group words and packing the tile's 4-bit valid counts in the same pass
   uint64_t* tw = ws.tilew + li * ws.tcap;
   const int ntiles = (ng + kGroupsPerTile - 1) / kGroupsPerTile;
   for (int t = tid; t < ntiles; t += kBuildThreads) {
+    const int g0 = t * kGroupsPerTile, g1 = min(ng, g0 + kGroupsPerTile);
+    int r = 0;
+    if (g0 < ng_real) {
+      int lo = 0, hi = nrun - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (run_g[mid] <= g0) lo = mid; else hi = mid - 1;
+      }
+      r = lo;
+    }
     uint64_t word = 0;
-    for (int q = 0; q < kGroupsPerTile && t * kGroupsPerTile + q < ng; ++q)
-      word |= uint64_t(group_at(t * kGroupsPerTile + q).y) << (4 * q);
+    for (int gi = g0; gi < g1; ++gi) {
+      int2 gw;
+      if (gi >= ng_real) {
+        gw = make_int2(rowbase + run_s[0], 0);  // the padding group: valid rows, all masked
+      } else {
+        while (run_g[r + 1] <= gi) ++r;  // run_g[nrun] = ng_real > gi
+        const int row = run_s[r] + 8 * (gi - run_g[r]);
+        gw = make_int2(rowbase + row, min(8, run_e[r] - row));
+      }
+      grp[gi] = gw;
+      word |= uint64_t(gw.y) << (4 * (gi - g0));
+    }
     tw[t] = word;
   }
 }
