@@ -12,6 +12,9 @@ namespace {
 
 constexpr long long kMaxN = 1ll << 24;
 constexpr int kMaxHostChunks = 64;
+// host pipeline: device staging slots (chunk ci uses slot ci % kHostSlots) and compute streams (env
+// SVG2_HOST_COMPUTE_STREAMS, at most kHostSlots)
+constexpr int kHostSlots = 3, kHostComputeStreams = 3;  // e2e HunyuanVideo: 62.7 / 57.9 / 57.5 ms with 1 / 2 / 3
 constexpr int kHostChunks = 6;  // middle chunks of the host pipeline (e2e, HunyuanVideo, one compute stream: 67.1 / 63.4 / 63.1 / 61.7 ms with 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; two compute streams: 59.7 / 57.5 / 58.4 ms with 4 / 6 / 9; env SVG2_HOST_CHUNKS / SVG2_HOST_RAMP override)
 
 svg2_status_t check_device() {
@@ -259,21 +262,20 @@ HostPlan host_plan(const svg2_dims_t& dm) {
   return p;
 }
 struct HostWs {
-  void *Q[2], *K[2], *V[2], *O[2];
-  FusedWs fused[2];  // one per compute stream: consecutive chunks run concurrently
+  void *Q[kHostSlots], *K[kHostSlots], *V[kHostSlots], *O[kHostSlots];
+  FusedWs fused[kHostSlots];  // one per compute stream: consecutive chunks run concurrently
 };
 HostWs carve_host(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg, const HostPlan& p) {
   HostWs w;
   const size_t q = size_t(p.hc) * dm.Nq * dm.d, k = size_t(p.hc) * dm.Nk * dm.d;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kHostSlots; ++i) {
     w.Q[i] = c.take<uint16_t>(q);
     w.K[i] = c.take<uint16_t>(k);
     w.V[i] = c.take<uint16_t>(k);
     w.O[i] = c.take<uint16_t>(q);
   }
   const svg2_dims_t chunk{1, p.hc, dm.Nq, dm.Nk, dm.d};
-  w.fused[0] = carve_fused(c, chunk, cfg);
-  w.fused[1] = carve_fused(c, chunk, cfg);
+  for (int i = 0; i < kHostSlots; ++i) w.fused[i] = carve_fused(c, chunk, cfg);
   return w;
 }
 }  // namespace
@@ -486,15 +488,15 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   // chunk and slot.  The k-means++ cold start (cooperative launches) keeps one compute stream.
   static const int compute_streams_env = [] {
     const char* v = getenv("SVG2_HOST_COMPUTE_STREAMS");
-    return v ? atoi(v) : 2;
+    return v ? atoi(v) : kHostComputeStreams;
   }();
   const bool pp_cold = !(cfg->flags & SVG2_WARM_START) && (cfg->flags & SVG2_INIT_KMEANSPP);
-  const int ncomp = (compute_streams_env >= 2 && !pp_cold) ? 2 : 1;
-  cudaStream_t sin = nullptr, scomp[2] = {nullptr, nullptr}, sout = nullptr;
+  const int ncomp = pp_cold ? 1 : (compute_streams_env < 1 ? 1 : (compute_streams_env > kHostSlots ? kHostSlots
+                                                                                                     : compute_streams_env));
+  cudaStream_t sin = nullptr, scomp[kHostSlots] = {}, sout = nullptr;
   cudaEvent_t start = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&scomp[0], cudaStreamNonBlocking);
-  if (e == cudaSuccess && ncomp == 2) e = cudaStreamCreateWithFlags(&scomp[1], cudaStreamNonBlocking);
+  for (int i = 0; i < ncomp && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&scomp[i], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
   const int n = plan.nchunks;
@@ -508,10 +510,10 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, start, 0);
   const size_t qrow = size_t(dm.Nq) * dm.d * 2, krow = size_t(dm.Nk) * dm.d * 2;  // bytes per head
   for (int ci = 0; e == cudaSuccess && ci < n; ++ci) {
-    const int bh0 = plan.start[ci], nh = plan.start[ci + 1] - bh0, slot = ci & 1;
-    cudaStream_t sc = scomp[ncomp == 2 ? slot : 0];
+    const int bh0 = plan.start[ci], nh = plan.start[ci + 1] - bh0, slot = ci % kHostSlots, cs = ci % ncomp;
+    cudaStream_t sc = scomp[cs];
     cudaEvent_t in = ev[3 * ci], done = ev[3 * ci + 1], out = ev[3 * ci + 2];
-    if (ci >= 2) e = cudaStreamWaitEvent(sin, ev[3 * (ci - 2) + 1], 0);  // slot's inputs consumed
+    if (ci >= kHostSlots) e = cudaStreamWaitEvent(sin, ev[3 * (ci - kHostSlots) + 1], 0);  // slot's inputs consumed
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.Q[slot], static_cast<const uint8_t*>(Qh) + bh0 * qrow, nh * qrow, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaEventRecord(evqk[2 * ci], sin);
@@ -521,13 +523,14 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.V[slot], static_cast<const uint8_t*>(Vh) + bh0 * krow, nh * krow, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaEventRecord(in, sin);
-    if (e == cudaSuccess && ci >= 2) e = cudaStreamWaitEvent(sc, ev[3 * (ci - 2) + 2], 0);  // slot's output read
+    if (e == cudaSuccess && ci >= kHostSlots)
+      e = cudaStreamWaitEvent(sc, ev[3 * (ci - kHostSlots) + 2], 0);  // slot's output read
     if (e == cudaSuccess) {
       const svg2_dims_t cd{1, nh, dm.Nq, dm.Nk, dm.d};
       const cudaEvent_t arrive[3] = {evqk[2 * ci], evqk[2 * ci + 1], in};  // the computation starts on Q alone
       e = run_fused(w.Q[slot], w.K[slot], w.V[slot], cd, cfg, q_centroids + size_t(bh0) * cfg->Cq * dm.d,
                     k_centroids + size_t(bh0) * cfg->Ck * dm.d, w.O[slot],
-                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused[ncomp == 2 ? slot : 0], sc, bh0,
+                    selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused[cs], sc, bh0,
                     arrive);
     }
     if (e == cudaSuccess) e = cudaEventRecord(done, sc);
@@ -540,7 +543,7 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   // compute events as well, so no work of either compute stream outlives the call
   if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 2], 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, ev[3 * (n - 1) + 1], 0);
-  if (e == cudaSuccess && n >= 2) e = cudaStreamWaitEvent(caller, ev[3 * (n - 2) + 1], 0);
+  for (int k = 2; k <= ncomp && k <= n && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(caller, ev[3 * (n - k) + 1], 0);
   for (int i = 0; i < 3 * n; ++i)
     if (ev[i]) cudaEventDestroy(ev[i]);
   for (int i = 0; i < 2 * n; ++i)
@@ -549,7 +552,7 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   delete[] evqk;
   if (start) cudaEventDestroy(start);
   if (sin) cudaStreamDestroy(sin);  // released once their queued work completes
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < kHostSlots; ++i)
     if (scomp[i]) cudaStreamDestroy(scomp[i]);
   if (sout) cudaStreamDestroy(sout);
   return from_cuda(e);
