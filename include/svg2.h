@@ -171,8 +171,8 @@ SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const
  * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (small first and last ones,
  * then 6 equal middle ones): the copy of
  * chunk c+1 to the device and of chunk c-1 back to the host overlap the computation of chunk c, consecutive chunks
- * compute on two alternating streams, and each role of a chunk waits only for its own tensor's upload (internal
- * streams, double-buffered device staging and two fused-call workspaces in the workspace,
+ * compute on three rotating streams, and each role of a chunk waits only for its own tensor's upload (internal
+ * streams, three device staging slots and three fused-call workspaces in the workspace,
  * SVG2_ENTRY_SPARSE_ATTENTION_HOST).  The centroid caches and
  * selected_pairs are DEVICE buffers as in svg2_sparse_attention.  The work is ordered after the work already queued
  * on `stream`, and later work on `stream` waits for it; Oh is complete when `stream` has synchronised. */

@@ -483,9 +483,10 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   Carver c(ws);
   HostWs w = carve_host(c, dm, *cfg, plan);
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
-  // four internal streams: copies in, two compute streams (chunk parity: the next chunk's k-means, selection and first
-  // attention items fill the SMs the current chunk's attention tail leaves idle), copies out; events order them per
-  // chunk and slot.  The k-means++ cold start (cooperative launches) keeps one compute stream.
+  // internal streams: copies in, up to kHostSlots compute streams (chunk ci on stream ci % ncomp: the next chunks'
+  // k-means, selection and first attention items fill the SMs the current chunk's attention tail leaves idle), copies
+  // out; events order them per chunk and slot.  The k-means++ cold start (cooperative launches) keeps one compute
+  // stream.
   static const int compute_streams_env = [] {
     const char* v = getenv("SVG2_HOST_COMPUTE_STREAMS");
     return v ? atoi(v) : kHostComputeStreams;
