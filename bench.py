@@ -361,6 +361,26 @@ def run_ours(args, wl):
     t_b2b_local = start2.elapsed_time(stop2) / args.steps
     t_b2b = reduce_scalar(t_b2b_local, "max")
     t_use = min(t_call, t_b2b)
+    multi = None
+    if world > 1:  # SURVEY 8(e) reporting: per-rank ms, imbalance, the call without the all-to-all
+        on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+        mine = torch.tensor([t_b2b_local], dtype=torch.float64, device=on)
+        allr = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [float(t.item()) for t in allr]
+        Qh, Kh, Vh = (seq_to_heads(t, assignment) for t in (Qs, Ks, Vs)) if assignment is not None else (Q, K, V)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s4, e4 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s4.record()
+        for _ in range(args.steps):
+            svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, fp8=fp8)
+        e4.record()
+        torch.cuda.synchronize()
+        t_noa2a = reduce_scalar(s4.elapsed_time(e4) / args.steps, "max")
+        multi = {"per_rank_ms": per_rank, "imbalance_max_over_mean": max(per_rank) / (sum(per_rank) / world),
+                 "ms_without_all_to_all": t_noa2a, "all_to_all_share": 1.0 - t_noa2a / t_b2b if t_b2b > 0 else None,
+                 "heads_per_rank": Hl}
 
     pairs_local = float(pairs.double().sum().item())
     pairs_total = reduce_scalar(pairs_local, "sum")
@@ -464,7 +484,7 @@ def run_ours(args, wl):
             "stages_ms": stage_ms, "gpu_launches": launches, "roofline": roofline, "e2e": e2e,
             "dense_baseline": dense, "cpu_baseline": cpu, "clocks": clocks.summary(),
             "attention_executed_tflops": achieved, "tile_work_multiplier": tile_work,
-            "head_assignment": assignment,
+            "head_assignment": assignment, "multi_gpu": multi,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,0 +1,79 @@
+"""The head-parallel multi-rank path end to end on one GPU (SURVEY 8(e) bitwise invariant): two ranks (gloo, the
+Ulysses all-to-all staged through host memory, both ranks on cuda:0) take token-sharded Q/K/V, reshard to their heads
+(dist.seq_to_head), run the fused SVG2 call (cold, then warm from their own centroid caches) and reshard O back
+(dist.head_to_seq).  The gathered output equals the one-process call on all heads bit for bit, for the cold and the
+warm call.  (NCCL over NVLink needs one GPU per rank; the index math and the kernels are the same.)"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+B, H, N, D, CQ, CK, ITERS, TOP_P = 1, 4, 2000, 128, 12, 20, 3, 0.9
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _inputs():
+    from gpu_helpers import random_qkv
+    q, k, v = random_qkv(B, H, N, N, D, seed=77)
+    return [torch.from_numpy(a.view(np.int16)).view(torch.bfloat16) for a in (q, k, v)]  # CPU [B,H,N,d]
+
+
+def _worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2505_18875_b200 as svg2
+        from paper_2505_18875_b200.dist import head_to_seq, seq_to_head
+        torch.cuda.set_device(0)
+        Q, K, V = (t.cuda() for t in _inputs())
+        n = N // world
+        # the sequence-parallel activations a DiT rank holds: [B, N/P, H, d], its token chunk, all heads
+        Qs, Ks, Vs = (t.permute(0, 2, 1, 3)[:, rank * n:(rank + 1) * n].contiguous() for t in (Q, K, V))
+        Qh, Kh, Vh = seq_to_head(Qs), seq_to_head(Ks), seq_to_head(Vs)
+        O1, _, ex = svg2.sparse_attention(Qh, Kh, Vh, CQ, CK, ITERS, TOP_P)
+        O2, _, _ = svg2.sparse_attention(Qh, Kh, Vh, CQ, CK, 2, TOP_P, ex["q_centroids"], ex["k_centroids"], warm=True)
+        torch.cuda.synchronize()
+        # plain numpy bytes through the queue (torch tensors would travel as shared-memory handles of this process)
+        out_q.put((rank, head_to_seq(O1).cpu().view(torch.int16).numpy().copy(),
+                   head_to_seq(O2).cpu().view(torch.int16).numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_equal_one_process_bitwise():
+    import paper_2505_18875_b200 as svg2
+    Q, K, V = (t.cuda() for t in _inputs())
+    O1, _, ex = svg2.sparse_attention(Q, K, V, CQ, CK, ITERS, TOP_P)
+    O2, _, _ = svg2.sparse_attention(Q, K, V, CQ, CK, 2, TOP_P, ex["q_centroids"], ex["k_centroids"], warm=True)
+    torch.cuda.synchronize()
+    ref1, ref2 = (o.permute(0, 2, 1, 3).cpu() for o in (O1, O2))  # token-major [B, N, H, d]
+    world = 2
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [out_q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = N // world
+    for rank, o1, o2 in got:
+        o1, o2 = (torch.from_numpy(a).view(torch.bfloat16) for a in (o1, o2))
+        assert torch.equal(o1, ref1[:, rank * n:(rank + 1) * n].contiguous()), f"cold call, rank {rank}"
+        assert torch.equal(o2, ref2[:, rank * n:(rank + 1) * n].contiguous()), f"warm call, rank {rank}"
