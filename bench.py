@@ -245,7 +245,7 @@ def run_ours(args, wl):
 
     top_p = args.top_p if args.top_p is not None else wl.top_p
     from paper_2505_18875_b200.dist import (balanced_assignment, head_range, head_to_seq, heads_to_seq, seq_to_head,
-                                            seq_to_heads)
+                                            seq_to_head_overlapped, seq_to_heads)
     h0, h1 = head_range(wl.H, rank, world)
     Hl = h1 - h0
     # inputs: this rank's heads, full sequence (synthetic, seeded per head)
@@ -303,15 +303,23 @@ def run_ours(args, wl):
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
 
+    # N > 1: Q, K, V resharded one after the other on a communication stream; the SVG2 call starts on Q while K and V
+    # are in flight (svg2_sparse_attention_ex input events; env SVG2_BENCH_OVERLAP=0 reshards all three first)
+    overlap = world > 1 and os.environ.get("SVG2_BENCH_OVERLAP", "1") != "0"
+    comm = torch.cuda.Stream() if overlap else None
+
     def step(events=None):
+        ready = None
         if assignment is not None:
             Qh, Kh, Vh = (seq_to_heads(t, assignment) for t in (Qs, Ks, Vs))
+        elif overlap:
+            (Qh, Kh, Vh), ready = seq_to_head_overlapped((Qs, Ks, Vs), comm)
         elif world > 1:
             Qh, Kh, Vh = seq_to_head(Qs), seq_to_head(Ks), seq_to_head(Vs)
         else:
             Qh, Kh, Vh = Q, K, V
         Oh, pr, _ = svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, cq, ck, warm=True, events=events,
-                                          fp8=fp8)
+                                          fp8=fp8, input_ready=ready)
         if assignment is not None:
             return heads_to_seq(Oh, assignment, wl.H), pr
         if world > 1:

@@ -166,6 +166,17 @@ SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const
                                     int64_t* selected_pairs, const svg2_debug_t* dbg, void* ws, size_t ws_bytes,
                                     void* stream);
 
+/* ---- The fused call with inputs still arriving (e.g. the Ulysses all-to-all of Q, K, V running on another stream):
+ * as svg2_sparse_attention, plus input_ready = NULL or three cudaEvent_t (as void*) recorded when Q, K and V are
+ * complete in device memory.  The Q-role k-means waits for Q's event, the K-role for K's, and V is waited for only
+ * before the pass that gathers it, so the computation overlaps the transfer of the later tensors.  A NULL event in a
+ * non-NULL input_ready is SVG2_ERR_NULL_POINTER.  svg2_sparse_attention(...) == svg2_sparse_attention_ex(..., NULL,
+ * ...). */
+SVG2_API svg2_status_t svg2_sparse_attention_ex(const void* Q, const void* K, const void* V, svg2_dims_t dims,
+                                                const svg2_config_t* config, float* q_centroids, float* k_centroids,
+                                                void* O, int64_t* selected_pairs, const svg2_debug_t* dbg,
+                                                void* const* input_ready, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- The fused call on HOST buffers (offload / end-to-end use).  Qh, Kh, Vh [B,H,N,d] bf16 and Oh [B,H,Nq,d] bf16
  * in host memory (page-locked for the copies to overlap; pageable memory works but serialises).  Same math and
  * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (small first and last ones,

@@ -29,7 +29,7 @@ STATUS = ["SVG2_OK", "SVG2_ERR_NULL_POINTER", "SVG2_ERR_INVALID_SHAPE", "SVG2_ER
           "SVG2_ERR_NOT_IMPLEMENTED"]
 EXPORTED_SYMBOLS = ["svg2_status_string", "svg2_abi_version", "svg2_workspace_size", "svg2_kmeans", "svg2_permute",
                     "svg2_select_topp", "svg2_varblock_attention", "svg2_unpermute", "svg2_sparse_attention",
-                    "svg2_sparse_attention_host", "svg2_sparse_attention_launch_count"]
+                    "svg2_sparse_attention_host", "svg2_sparse_attention_launch_count", "svg2_sparse_attention_ex"]
 
 
 class SVG2Error(RuntimeError):
@@ -82,11 +82,13 @@ def load_library(path: str = LIB_PATH):
     lib.svg2_unpermute.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
     lib.svg2_sparse_attention.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp,
                                           ctypes.POINTER(Debug), vp, sz, vp]
+    lib.svg2_sparse_attention_ex.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp,
+                                             ctypes.POINTER(Debug), ctypes.POINTER(vp), vp, sz, vp]
     lib.svg2_sparse_attention_host.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_sparse_attention_launch_count.argtypes = [Dims, ctypes.POINTER(Config)]
     lib.svg2_sparse_attention_launch_count.restype = i32
     for name in ["svg2_kmeans", "svg2_permute", "svg2_select_topp", "svg2_varblock_attention", "svg2_unpermute",
-                 "svg2_sparse_attention", "svg2_sparse_attention_host"]:
+                 "svg2_sparse_attention", "svg2_sparse_attention_ex", "svg2_sparse_attention_host"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -258,11 +260,13 @@ def launch_count(B, H, Nq, Nk, d, Cq, Ck, iters, top_p, warm, init: str = "strid
 
 def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_centroids=None, k_centroids=None,
                      warm: bool = False, scale: float = 0.0, debug: bool = False, events=None, out=None,
-                     init: str = "strided", seed: int = 0, fp8: bool = False):
+                     init: str = "strided", seed: int = 0, fp8: bool = False, input_ready=None):
     """The fused SVG2 call.  Q, K, V [B,H,N,d] bf16 CUDA.  q_centroids [B,H,Cq,d] / k_centroids [B,H,Ck,d] f32 are
     the centroid caches (read iff warm, always written).  Cold calls start k-means from `init` ("strided" or
     "kmeans++" with `seed`, R25).  Returns (O, selected_pairs, extras) where extras holds
-    the centroids and, if debug, the intermediates (labels, perms, offsets, mask)."""
+    the centroids and, if debug, the intermediates (labels, perms, offsets, mask).  input_ready: None or three
+    torch.cuda.Event recorded when Q, K and V are complete (svg2_sparse_attention_ex): the computation on Q starts
+    while K and V are still arriving."""
     lib = load_library()
     for t, n in ((Q, "Q"), (K, "K"), (V, "V")):
         _need(t, torch.bfloat16, n, 4)
@@ -307,10 +311,19 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
                 if not ev.cuda_event:  # torch creates events lazily: record once so a handle exists
                     ev.record()
                 dbg.events[i] = ev.cuda_event
+    ready = None
+    if input_ready is not None:
+        if len(input_ready) != 3:
+            raise ValueError("input_ready: three events (Q, K, V)")
+        ready = (ctypes.c_void_p * 3)(*[ev.cuda_event for ev in input_ready])
+        if not all(ready):
+            raise ValueError("input_ready: record every event before the call")
     _check("svg2_sparse_attention",
-           lib.svg2_sparse_attention(_p(Q), _p(K), _p(V), dims, ctypes.byref(cfg), _p(q_centroids), _p(k_centroids),
-                                     _p(O), _p(pairs), ctypes.byref(dbg) if dbg is not None else None, _p(ws),
-                                     ws.numel(), _stream()))
+           lib.svg2_sparse_attention_ex(_p(Q), _p(K), _p(V), dims, ctypes.byref(cfg), _p(q_centroids),
+                                        _p(k_centroids), _p(O), _p(pairs),
+                                        ctypes.byref(dbg) if dbg is not None else None,
+                                        ctypes.cast(ready, ctypes.POINTER(ctypes.c_void_p)) if ready else None,
+                                        _p(ws), ws.numel(), _stream()))
     return O, pairs, extras
 
 

@@ -451,6 +451,15 @@ svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V,
                                     const svg2_config_t* cfg, float* q_centroids, float* k_centroids, void* O,
                                     int64_t* selected_pairs, const svg2_debug_t* dbg, void* ws, size_t ws_bytes,
                                     void* stream) {
+  return svg2_sparse_attention_ex(Q, K, V, dm, cfg, q_centroids, k_centroids, O, selected_pairs, dbg, nullptr, ws,
+                                  ws_bytes, stream);
+}
+
+svg2_status_t svg2_sparse_attention_ex(const void* Q, const void* K, const void* V, svg2_dims_t dm,
+                                       const svg2_config_t* cfg, float* q_centroids, float* k_centroids, void* O,
+                                       int64_t* selected_pairs, const svg2_debug_t* dbg, void* const* input_ready,
+                                       void* ws, size_t ws_bytes, void* stream) {
+  if (input_ready && (!input_ready[0] || !input_ready[1] || !input_ready[2])) return SVG2_ERR_NULL_POINTER;
   if (!Q || !K || !V || !cfg || !q_centroids || !k_centroids || !O || !ws) return SVG2_ERR_NULL_POINTER;
   svg2_status_t st = validate_fused(dm, cfg);
   if (st != SVG2_OK) return st;
@@ -463,8 +472,11 @@ svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V,
 
   Carver c(ws);
   FusedWs w = carve_fused(c, dm, *cfg);
+  cudaEvent_t ready[3];
+  if (input_ready)
+    for (int i = 0; i < 3; ++i) ready[i] = static_cast<cudaEvent_t>(input_ready[i]);
   return from_cuda(run_fused(Q, K, V, dm, cfg, q_centroids, k_centroids, O, selected_pairs, dbg, w,
-                             static_cast<cudaStream_t>(stream), 0));
+                             static_cast<cudaStream_t>(stream), 0, input_ready ? ready : nullptr));
 }
 
 svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const void* Vh, svg2_dims_t dm,

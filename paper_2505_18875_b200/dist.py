@@ -62,6 +62,27 @@ def head_to_seq(y: torch.Tensor, group=None) -> torch.Tensor:
 # resident on their rank.
 
 
+def seq_to_head_overlapped(xs, comm_stream: torch.cuda.Stream, group=None):
+    """seq_to_head of several tensors (Q, K, V) on `comm_stream`, one after the other, so that the SVG2 call can start
+    on the first while the others are in flight: returns the head-sharded tensors and one CUDA event per tensor,
+    recorded when it is complete (for sparse_attention(..., input_ready=events), svg2_sparse_attention_ex).  The
+    returned tensors are marked as used by the current stream (caching-allocator safety)."""
+    cur = torch.cuda.current_stream()
+    comm_stream.wait_stream(cur)
+    outs, events = [], []
+    with torch.cuda.stream(comm_stream):
+        for x in xs:
+            x.record_stream(comm_stream)
+            y = seq_to_head(x, group)
+            ev = torch.cuda.Event()
+            ev.record(comm_stream)
+            outs.append(y)
+            events.append(ev)
+    for y in outs:
+        y.record_stream(cur)
+    return outs, events
+
+
 def balanced_assignment(costs, world: int):
     """Heads -> ranks with near-equal total cost: heads in decreasing cost (ties: lower index first), each to the
     least-loaded rank (ties: lower rank).  Returns a list of sorted head lists, one per rank."""
