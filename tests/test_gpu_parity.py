@@ -362,10 +362,36 @@ def test_abi_errors(svg2):
     with pytest.raises(svg2.SVG2Error) as e:
         svg2.sparse_attention(bad, bad, bad, 8, 8, 1, 0.9)
     assert e.value.status == 2
+    # svg2_sparse_attention_ex: a NULL event inside a non-NULL input_ready array is rejected before any launch
+    import ctypes
+    lib = svg2.load_library()
+    cfg = svg2.Config(8, 8, 1, 0.9, 0.0, 0, 0)
+    dims = svg2.Dims(1, 1, 256, 256, 64)
+    qc = torch.empty(1, 1, 8, 64, dtype=torch.float32, device="cuda")
+    kc = torch.empty_like(qc)
+    O0 = torch.zeros_like(Q)
+    nbytes = int(lib.svg2_workspace_size(svg2.ENTRY_SPARSE_ATTENTION, dims, ctypes.byref(cfg)))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    ev = torch.cuda.Event()
+    ev.record()
+    ready = (ctypes.c_void_p * 3)(ev.cuda_event, None, ev.cuda_event)
+    st = lib.svg2_sparse_attention_ex(Q.data_ptr(), K.data_ptr(), V.data_ptr(), dims, ctypes.byref(cfg), qc.data_ptr(),
+                                      kc.data_ptr(), O0.data_ptr(), None, None,
+                                      ctypes.cast(ready, ctypes.POINTER(ctypes.c_void_p)), ws.data_ptr(), nbytes, None)
+    assert st == 1  # SVG2_ERR_NULL_POINTER
+    torch.cuda.synchronize()
+    assert not O0.any()  # nothing was enqueued
     # the library still works after the rejected calls
     O, _, _ = svg2.sparse_attention(Q, K, V, 8, 8, 1, 0.9)
     torch.cuda.synchronize()
     assert torch.isfinite(O.float()).all()
+    # and with input events that are all recorded, _ex equals the plain call bitwise
+    e3 = [torch.cuda.Event() for _ in range(3)]
+    for e_ in e3:
+        e_.record()
+    O2, _, _ = svg2.sparse_attention(Q, K, V, 8, 8, 1, 0.9, input_ready=e3)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O2)
 
 
 # ------------------------------------------------------------------ full size, bench launch configuration
