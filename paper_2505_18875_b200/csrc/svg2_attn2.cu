@@ -731,7 +731,9 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
   };
   if constexpr (D == 128) {
     if (fp8) {
-      launch(k_varblock_attn<D, kDefaultPoly, true>, Cfg<D>::kSmemBytesFp8);
+      if (poly == 2) launch(k_varblock_attn<D, 2, true>, Cfg<D>::kSmemBytesFp8);
+      else if (poly == 6) launch(k_varblock_attn<D, 6, true>, Cfg<D>::kSmemBytesFp8);
+      else launch(k_varblock_attn<D, kDefaultPoly, true>, Cfg<D>::kSmemBytesFp8);
       return cudaGetLastError();
     }
   }
