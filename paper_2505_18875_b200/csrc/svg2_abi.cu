@@ -112,6 +112,15 @@ static bool role_streams_enabled() {
   return on;
 }
 
+// env SVG2_ROLE_PRIO=0: the forked (K-role) stream at the lowest priority instead of the highest (measurement)
+static bool role_prio_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SVG2_ROLE_PRIO");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 // The whole fused call for the heads of `dm` on stream s (arguments validated by the caller).  bh_base = global
 // (b,h) index of the first head (k-means++ stream ids of chunked calls, R25).
 cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_dims_t& dm, const svg2_config_t* cfg,
@@ -156,13 +165,18 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
       gk.Yp = w.Vp;
     }
   }
-  // Q role on a forked stream, K role on s; the k-means++ cold start (cooperative launches) stays on one stream
+  // The K role (the longer one: C_k > C_q) on a forked stream of the highest priority, enqueued first, so that its
+  // kernels win the SMs whenever both roles have work ready; the Q role on s.  The k-means++ cold start (cooperative
+  // launches) stays on one stream.
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStreamCaptureStatus capture = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &capture);  // inside a graph capture: stay on the caller's stream (no stream creation)
   if (role_streams_enabled() && !(!warm && init_q.kmeanspp) && capture == cudaStreamCaptureStatusNone) {
-    if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+    int prio_low = 0, prio_high = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, role_prio_enabled() ? prio_high : prio_low) !=
+            cudaSuccess ||
         cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventRecord(ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(s2, ev_fork, 0) != cudaSuccess) {
@@ -171,17 +185,18 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
       (void)cudaGetLastError();
     }
   }
+  cudaStream_t sk = s2 ? s2 : s;  // K role
   if (arrive) {
-    cudaStreamWaitEvent(s2 ? s2 : s, arrive[0], 0);
+    cudaStreamWaitEvent(sk, arrive[1], 0);
     if (gk.Yp) gk.wait_y = arrive[2];
   }
-  e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q, w.off_q,
-                    w.km_q, s2 ? s2 : s, nullptr, init_q, gq);
+  e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k, w.off_k,
+                    w.km_k, sk, nullptr, init_k, gk);
   mark(1);  // with two streams: the fork point (stage "kmeans_k" then covers both roles)
-  if (arrive) cudaStreamWaitEvent(s, arrive[1], 0);
+  if (arrive) cudaStreamWaitEvent(s, arrive[0], 0);
   if (e == cudaSuccess)
-    e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k,
-                      w.off_k, w.km_k, s, nullptr, init_k, gk);
+    e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q,
+                      w.off_q, w.km_q, s, nullptr, init_q, gq);
   if (s2) {  // join (always, so no work is left behind on s2 even after an error) and release (deferred by CUDA)
     cudaEventRecord(ev_join, s2);
     cudaStreamWaitEvent(s, ev_join, 0);
