@@ -158,7 +158,8 @@ SVG2_API svg2_status_t svg2_unpermute(const void* Op, const int32_t* perm, int32
  * f32, read iff config->flags & SVG2_WARM_START, always written back), permutation, selection, variable-block
  * attention with the unpermute fused into its epilogue.  O [B,H,Nq,d] bf16 out in original token order.
  * selected_pairs [B,H] int64 out (nullable).  dbg: NULL or intermediates / stage events (see svg2_debug_t).
- * Streams: the Q-role k-means runs on a stream forked from `stream` for the duration of the call (event fork /
+ * Streams: the K-role k-means runs on a (high-priority) stream forked from `stream` for the duration of the call
+ * (event fork /
  * join, created and released per call; not while `stream` is being captured into a CUDA graph, where the call
  * stays on `stream` and is capture-safe); all work is ordered after, and joined back into, `stream`. */
 SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V, svg2_dims_t dims,
