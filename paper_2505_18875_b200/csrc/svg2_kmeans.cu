@@ -179,21 +179,24 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         const int as = ac % kAccStages;
         mbar_wait(&bars.acc_full[as], (ac / kAccStages) & 1);
         tc_fence_after();
+        // all four 32-column loads of the stage in flight before one wait (one TMEM round trip per chunk, not four)
+        uint32_t r4[kCentChunk / 32][32];
+#pragma unroll
+        for (int q = 0; q < kCentChunk / 32; ++q) tmem_ld32(tmem + lane_addr + as * 128 + 32 * q, r4[q]);
+        tmem_wait_ld();
 #pragma unroll
         for (int q = 0; q < kCentChunk / 32; ++q) {
-          uint32_t r[32];
-          tmem_ld32(tmem + lane_addr + as * 128 + 32 * q, r);
-          tmem_wait_ld();
           const int j0 = c * kCentChunk + 32 * q;
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const float dist = fmaf(-2.f, __uint_as_float(r[e]), sNorm[j0 + e]);
+            const float dist = fmaf(-2.f, __uint_as_float(r4[q][e]), sNorm[j0 + e]);
             if (dist < best) {  // strict: ties keep the lower index
               best = dist;
               bj = j0 + e;
             }
           }
         }
+        // released after the argmin (releasing right after the loads measured slower: 594 vs 574 us per K launch)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.acc_empty[as]);
