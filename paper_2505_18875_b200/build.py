@@ -27,7 +27,7 @@ def needs_build():
 
 
 def build(force=False, verbose=False, out=None, defines=()):
-    """out/defines: build a variant library (e.g. the cycle-trace build) without touching the product .so."""
+    """out/defines: build a variant library (e.g. with -DSVG2_WATCHDOG_PRINTF) without touching the product .so."""
     lib = out or LIB
     if not force and out is None and not needs_build():
         return LIB
@@ -65,7 +65,4 @@ def build(force=False, verbose=False, out=None, defines=()):
 
 
 if __name__ == "__main__":
-    if "--trace" in sys.argv:  # cycle-trace variant for SVG2_DEBUG_MODE=2 (loaded via SVG2_LIBRARY)
-        build(force=True, out=os.path.join(ROOT, "build", "libsvg2_trace.so"), defines=("SVG2_TRACE_PRINT",))
-    else:
-        build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True)

@@ -12,8 +12,8 @@ constexpr int kQTile = 128;          // query rows per tcgen05 M=128 tile
 constexpr int kKTile = 128;          // keys per S tile (N of the QK^T MMA, K of the PV MMA)
 constexpr int kItemRows = 2 * kQTile;  // one attention work item = two Q tiles of one query cluster
 // Work item int4 = {first flat row of Q', rows_a | rows_b << 16, stream index, bh | flags}.  kItemSplit marks an
-// item with one Q tile and >= 2 key tiles: the v2 kernel gives its even key tiles to one softmax warpgroup and the
-// odd ones to the other and merges the two partial softmax states (other pipelines run it as a one-tile item).
+// item with one Q tile and >= 2 key tiles: the attention kernels give its even key tiles to one softmax warpgroup and
+// the odd ones to the other and merge the two partial softmax states.
 constexpr int kItemSplit = 1 << 30;
 constexpr int kItemBhMask = kItemSplit - 1;
 
@@ -75,9 +75,11 @@ inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
 // Key stream of one query cluster = its selected key clusters' rows in K'/V', adjacent clusters merged into runs,
 // every run padded to whole 8-row groups.  A group = (first row in the flattened [BH*Nk] key tensor, #valid rows
 // 0..8).  The stream is padded to an even number of groups so every tile has N = 16*k keys.  Tile t = groups
-// [16t, 16t+16); its 16 valid counts are also packed 4 bits each into one 64-bit tile word for the softmax mask.
+// [gpt t, gpt t + gpt) (gpt = attn_groups_per_tile: 10 or 16); its valid counts are also packed 4 bits each into one
+// 64-bit tile word for the softmax mask.  tile_cap covers the smallest tile (kMinGroupsPerTile groups).
+constexpr int kMinGroupsPerTile = 8;
 inline size_t group_cap(int Nk, int Ck) { return size_t(Nk) / 8 + size_t(Ck) + 2; }
-inline size_t tile_cap(int Nk, int Ck) { return group_cap(Nk, Ck) / 16 + 1; }
+inline size_t tile_cap(int Nk, int Ck) { return group_cap(Nk, Ck) / kMinGroupsPerTile + 1; }
 
 struct AttnWs {
   int2* groups;        // [BH, Cq, group_cap]
@@ -86,7 +88,7 @@ struct AttnWs {
   int4* items_bh;      // [BH, cap]
   int32_t* items_cnt;  // [BH]
   int4* items;         // [BH * cap] flattened
-  int32_t* n_items;    // [2]: item count, dynamic-scheduler counter
+  int32_t* n_items;    // [3]: item count, dynamic-scheduler counter, query rows with an empty key stream
   size_t gcap, tcap;
 };
 inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Nk, int Cq, int Ck) {
@@ -100,7 +102,7 @@ inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Nk, int Cq, int Ck) {
   w.items_bh = c.take<int4>(size_t(BH) * cap);
   w.items_cnt = c.take<int32_t>(BH);
   w.items = c.take<int4>(size_t(BH) * cap);
-  w.n_items = c.take<int32_t>(2);
+  w.n_items = c.take<int32_t>(3);
   return w;
 }
 
@@ -134,12 +136,20 @@ cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters,
 cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH,
                                int Cq, int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
                                cudaStream_t s);
+// The attention's output rows, for the NaN fill of query clusters with an empty key stream (k_items)
+struct OrphanFill {
+  const int32_t* q_perm;  // nullable: rows in permuted order
+  void* O;                // bf16 [BH, Nq, d]
+  float* lse;             // nullable
+  int d;
+};
+// key-stream tile size (8-row groups) the attention pipeline for (d, FP8 PV) runs on: the work list must match it
+int attn_groups_per_tile(int d, bool fp8);
 cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
-                                  int Nq, int Nk, int Cq, int Ck, AttnWs ws, cudaStream_t s);
-cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk,
-                                      int d, int Cq, int Ck, float scale, const int32_t* q_perm, void* O,
-                                      float* lse, AttnWs ws, cudaStream_t s,
-                                      const uint32_t* v_amax = nullptr);
+                                  int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s);
+cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
+                                      float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
+                                      cudaStream_t s, const uint32_t* v_amax = nullptr);
 int kmeans_launch_count(int iters, bool warm);
 cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
                             float* cent, void* ws, cudaStream_t s);

@@ -2,7 +2,6 @@
 // touched on error), workspace carving, and the enqueue of the kernels of svg2_*.cu on the caller's stream.
 #include <cuda_runtime.h>
 #include <cmath>
-#include <cstdlib>
 #include "../../include/svg2.h"
 #include "internal.h"
 
@@ -12,10 +11,13 @@ namespace {
 
 constexpr long long kMaxN = 1ll << 24;
 constexpr int kMaxHostChunks = 64;
-// host pipeline: device staging slots (chunk ci uses slot ci % kHostSlots) and compute streams (env
-// SVG2_HOST_COMPUTE_STREAMS, at most kHostSlots)
+// host pipeline: device staging slots (chunk ci uses slot ci % kHostSlots) and compute streams (<= kHostSlots)
 constexpr int kHostSlots = 3, kHostComputeStreams = 3;  // e2e HunyuanVideo: 62.7 / 57.9 / 57.5 ms with 1 / 2 / 3
-constexpr int kHostChunks = 6;  // middle chunks of the host pipeline (e2e, HunyuanVideo, one compute stream: 67.1 / 63.4 / 63.1 / 61.7 ms with 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; two compute streams: 59.7 / 57.5 / 58.4 ms with 4 / 6 / 9; env SVG2_HOST_CHUNKS / SVG2_HOST_RAMP override)
+// middle chunks of the host pipeline (e2e, HunyuanVideo, one compute stream: 67.1 / 63.4 / 63.1 / 61.7 ms with
+// 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; two compute streams: 59.7 / 57.5 / 58.4 ms with
+// 4 / 6 / 9)
+constexpr int kHostChunks = 6;
+static_assert(kHostChunks + 4 <= kMaxHostChunks, "host chunks");
 
 svg2_status_t check_device() {
   int dev = 0, major = 0, minor = 0;
@@ -93,34 +95,6 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
   return SVG2_OK;
 }
 
-// A6 fused into the last k-means update (default), or separate gather launches (env SVG2_FUSE_GATHER=0, measurement)
-static bool fuse_gather_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("SVG2_FUSE_GATHER");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
-// The Q and K k-means run on two streams (fork / join through events; env SVG2_ROLE_STREAMS=0: one stream) so the
-// latency-bound kernels of one role overlap the other role's
-static bool role_streams_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("SVG2_ROLE_STREAMS");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
-// env SVG2_ROLE_PRIO=0: the forked (K-role) stream at the lowest priority instead of the highest (measurement)
-static bool role_prio_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("SVG2_ROLE_PRIO");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
 // The whole fused call for the heads of `dm` on stream s (arguments validated by the caller).  bh_base = global
 // (b,h) index of the first head (k-means++ stream ids of chunked calls, R25).
 cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_dims_t& dm, const svg2_config_t* cfg,
@@ -155,15 +129,12 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   // A6 rides on the last Lloyd update: that pass already reads every row through the final permutation, so it also
   // writes Q' = pi_q Q, K' = pi_k K and (bf16 PV) V' = pi_k V
   const bool fp8 = (cfg->flags & SVG2_FP8_PV) != 0;
-  const bool fuse_gather = fuse_gather_enabled();
   KmeansGather gq, gk;
-  if (fuse_gather) {
-    gq.Xp = w.Qp;
-    gk.Xp = w.Kp;
-    if (!fp8) {
-      gk.Y = V;
-      gk.Yp = w.Vp;
-    }
+  gq.Xp = w.Qp;
+  gk.Xp = w.Kp;
+  if (!fp8) {
+    gk.Y = V;
+    gk.Yp = w.Vp;
   }
   // The K role (the longer one: C_k > C_q) on a forked stream of the highest priority, enqueued first, so that its
   // kernels win the SMs whenever both roles have work ready; the Q role on s.  The k-means++ cold start (cooperative
@@ -172,10 +143,10 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStreamCaptureStatus capture = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &capture);  // inside a graph capture: stay on the caller's stream (no stream creation)
-  if (role_streams_enabled() && !(!warm && init_q.kmeanspp) && capture == cudaStreamCaptureStatusNone) {
+  if (!(!warm && init_q.kmeanspp) && capture == cudaStreamCaptureStatusNone) {
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
-    if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, role_prio_enabled() ? prio_high : prio_low) !=
+    if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio_high) !=
             cudaSuccess ||
         cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
@@ -205,10 +176,7 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   mark(2);
-  if (arrive && !gk.wait_y) cudaStreamWaitEvent(s, arrive[2], 0);  // V gathered by a separate pass
-  if (e == cudaSuccess && !fuse_gather) e = launch_gather_rows(w.perm_q, BH, dm.Nq, dm.d, Q, w.Qp, nullptr, nullptr, s);
-  if (e == cudaSuccess && !fuse_gather)
-    e = launch_gather_rows(w.perm_k, BH, dm.Nk, dm.d, K, w.Kp, fp8 ? nullptr : V, w.Vp, s);
+  if (arrive && !gk.wait_y) cudaStreamWaitEvent(s, arrive[2], 0);  // V gathered by a separate pass (FP8 PV)
   // FP8 PV (R26): V' in e4m3 with a per-head scale, written into the first half of the bf16 V' buffer
   if (e == cudaSuccess && fp8) e = launch_gather_rows_e4m3(w.perm_k, BH, dm.Nk, dm.d, V, w.Vp, w.v_amax, s);
   mark(3);
@@ -217,11 +185,12 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
                            cfg->top_p, w.mask, selected_pairs, s);
   mark(4);
   if (e == cudaSuccess)
-    e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck, w.attn, s);
+    e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck,
+                              attn_groups_per_tile(dm.d, fp8), w.attn, OrphanFill{w.perm_q, O, nullptr, dm.d}, s);
   mark(5);
   if (e == cudaSuccess)
-    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, cfg->Cq, cfg->Ck, scale, w.perm_q, O,
-                                  nullptr, w.attn, s, fp8 ? w.v_amax : nullptr);
+    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, scale, w.perm_q, O, nullptr, w.attn, s,
+                                  fp8 ? w.v_amax : nullptr);
   mark(6);
   mark(7);
   return e;
@@ -236,22 +205,13 @@ struct HostPlan {
 // with computation, so the chunks ramp up 1, 2 heads at the start and down 2, 1 at the end around equal middle
 // chunks (kHostChunks of them); small problems get one chunk per head.
 HostPlan host_plan(const svg2_dims_t& dm) {
-  static const int chunks_env = [] {
-    const char* e = getenv("SVG2_HOST_CHUNKS");
-    return e ? atoi(e) : 0;
-  }();
-  static const int ramp_env = [] {
-    const char* e = getenv("SVG2_HOST_RAMP");
-    return e ? atoi(e) : 1;
-  }();
   HostPlan p;
   p.BH = dm.B * dm.H;
   int sizes[kMaxHostChunks], n = 0;
-  const int mid_want = chunks_env > 0 ? chunks_env : kHostChunks;
-  const int mid_chunks = mid_want < kMaxHostChunks - 4 ? mid_want : kMaxHostChunks - 4;
+  const int mid_chunks = kHostChunks;
   int rest = p.BH;
   const int ramp[2] = {1, 2};
-  const bool use_ramp = ramp_env != 0 && p.BH >= 2 * (ramp[0] + ramp[1]) + mid_chunks;
+  const bool use_ramp = p.BH >= 2 * (ramp[0] + ramp[1]) + mid_chunks;
   if (use_ramp) {
     sizes[n++] = ramp[0];
     sizes[n++] = ramp[1];
@@ -431,10 +391,11 @@ svg2_status_t svg2_varblock_attention(const void* Qp, const void* Kp, const void
   const int BH = dm.B * dm.H;
   AttnWs aw = carve_attn(c, BH, dm.Nq, dm.Nk, Cq, Ck);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_build_worklist(q_offsets, k_offsets, mask, BH, dm.Nq, dm.Nk, Cq, Ck, aw, s);
+  cudaError_t e = launch_build_worklist(q_offsets, k_offsets, mask, BH, dm.Nq, dm.Nk, Cq, Ck,
+                                        attn_groups_per_tile(dm.d, false), aw, OrphanFill{q_perm, O, lse, dm.d}, s);
   if (e == cudaSuccess)
-    e = launch_varblock_attention(Qp, Kp, Vp, BH, dm.Nq, dm.Nk, dm.d, Cq, Ck, resolve_scale(scale, dm.d), q_perm, O,
-                                  lse, aw, s);
+    e = launch_varblock_attention(Qp, Kp, Vp, BH, dm.Nq, dm.Nk, dm.d, resolve_scale(scale, dm.d), q_perm, O, lse,
+                                  aw, s);
   return from_cuda(e);
 }
 
@@ -455,7 +416,6 @@ int32_t svg2_sparse_attention_launch_count(svg2_dims_t dm, const svg2_config_t* 
   const bool warm = cfg->flags & SVG2_WARM_START;
   // the Q / K / V gathers are fused into the last k-means update (no launches of their own)
   int n = 2 * kmeans_launch_count(cfg->iters, warm) + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
-  if (!fuse_gather_enabled()) n += 2;
   if (cfg->flags & SVG2_FP8_PV) n += 2;  // |V| max per head + the e4m3 gather
   if (!warm && (cfg->flags & SVG2_INIT_KMEANSPP))
     n += kmeanspp_launch_count(dm.B * dm.H, dm.Nq, dm.d) + kmeanspp_launch_count(dm.B * dm.H, dm.Nk, dm.d) - 2;
@@ -514,13 +474,8 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
   // k-means, selection and first attention items fill the SMs the current chunk's attention tail leaves idle), copies
   // out; events order them per chunk and slot.  The k-means++ cold start (cooperative launches) keeps one compute
   // stream.
-  static const int compute_streams_env = [] {
-    const char* v = getenv("SVG2_HOST_COMPUTE_STREAMS");
-    return v ? atoi(v) : kHostComputeStreams;
-  }();
   const bool pp_cold = !(cfg->flags & SVG2_WARM_START) && (cfg->flags & SVG2_INIT_KMEANSPP);
-  const int ncomp = pp_cold ? 1 : (compute_streams_env < 1 ? 1 : (compute_streams_env > kHostSlots ? kHostSlots
-                                                                                                     : compute_streams_env));
+  const int ncomp = pp_cold ? 1 : kHostComputeStreams;
   cudaStream_t sin = nullptr, scomp[kHostSlots] = {}, sout = nullptr;
   cudaEvent_t start = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);

@@ -1,31 +1,24 @@
-// svg2_attn2.cu — A9 (+ fused A10), design v2 (128-key S tiles, single S/P buffer per Q tile): dynamic-block-size sparse attention over the permuted, cluster-contiguous
-// tokens, written for sm_100a.
+// svg2_attn_fp8.cu — A9 (+ fused A10) with the PV product in e4m3 (the "+FP8" variant of PAPER.md:414, 418; DESIGN
+// R26), written for sm_100a.  Same work list as svg2_attn.cu (key streams of 8-row groups), 128-key tiles.
 //
-// Work item = two 128-row Q tiles of one query cluster i (contiguous rows of Q' after the permutation) sharing ONE
-// packed key stream: the selected key clusters' row ranges of K'/V' (adjacent selected clusters merged into runs),
-// each run padded to whole 8-row groups.  The paper loads K/V "sparsely per token via address offsets into
-// contiguous shared memory"; here a 128-key tile of the stream (16 groups) is assembled from TMA box
-// loads straight into the 128B-swizzled layout the MMA descriptors expect: consecutive groups of one run merge into
-// power-of-two boxes of 8..128 rows, so a tile typically costs 1-3 box loads per 64-column half.  Padding rows of a
-// run's last group are masked in the softmax (a 4-bit valid count per group, packed per tile).
+// Work item = two 128-row Q tiles of one query cluster sharing one packed key stream (svg2_attn.cu).  V' arrives in
+// e4m3 (scale 448 / amax per head, computed by the permute step), P is packed to e4m3 in TMEM and PV runs as
+// kind::f8f6f4 MMAs (K = 32 keys each, half the instructions of bf16); QK^T, the softmax statistics and O stay
+// bf16 / fp32.  d = 128 only.
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter).  The warp
-// scheduler favours high warp ids, so the latency-critical single-thread MMA issuers get the highest ones:
+// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter):
 //   warps 0-3   softmax warpgroup for Q tile a; warps 4-7 for Q tile b.  One thread = one query row = one TMEM
-//               lane (warp w owns lanes 32(w%4)..+31): tcgen05.ld S, online softmax in registers (exp2 domain, lazy
-//               rescale when the running max grows by > 8), P (bf16) written back over S with tcgen05.st, O rescaled
-//               in TMEM when needed; epilogue O / l -> bf16 -> global, scattered to original token order through
-//               pi_q (fused A10).
-//   warp 8      scheduler + TMA producer: fetches the next item, broadcasts it through a 2-slot smem ring, loads the
-//               Q tiles and the K/V tiles (box loads) into 2-stage rings
+//               lane: tcgen05.ld S, online softmax in registers (exp2 domain, lazy rescale when the running max grows
+//               by > 8), P (e4m3) written back over S with tcgen05.st, O rescaled in TMEM when needed; epilogue
+//               O / l -> bf16 -> global, scattered to original token order through pi_q (fused A10).
+//   warp 8      scheduler + TMA producer (Q tiles, K tiles and e4m3 V tiles into 3-stage rings)
 //   warp 9      TMEM allocator (512 columns: S_a | S_b | O_a | O_b)
 //   warp 11     MMA issuer (whole warp convergent, elect.sync issues; highest priority), for both Q tiles in turn:
-//               S = Q K^T (SS, K-major both) into TMEM, then per key tile O += P V (TS: P read from TMEM, V MN-major)
+//               S = Q K^T (SS) into TMEM, then per key tile O += P V (TS: P read from TMEM, V MN-major)
 //               followed by the next S, which overwrites P only after the PV that reads it (in-order tensor pipe).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
-#include <cstdlib>
 #include "internal.h"
 #include "ptx.cuh"
 #include "tmap.h"
@@ -42,7 +35,7 @@ constexpr int kGroupsPerTile = kKTile / 8;  // 16
 constexpr int kBoxKinds = 5;                // box heights 8, 16, 32, 64, 128 rows
 // Lazy rescale threshold (log2 units): O and l are rescaled only when a row's tile max exceeds the max in use by
 // more than this, so P <= 2^threshold between rescales.  P is bf16 (relative precision at any magnitude) and O / l
-// accumulate in fp32, so 2^20 leaves > 10^20 headroom for 10^5 keys.  Env SVG2_RESCALE_LOG2 overrides (measurement).
+// accumulate in fp32, so 2^20 leaves > 10^20 headroom for 10^5 keys.
 constexpr float kRescaleThreshold = 8.0f;
 constexpr uint64_t kFullTileWord = 0x8888888888888888ull;
 // setmaxnreg budget: the launch reserves 168 regs x 384 threads; the control warpgroup (warps 8-11) shrinks to 72
@@ -90,29 +83,8 @@ struct Params {
   float* lse;
   int Nq;
   float scale_log2;
-  float rescale_thr;  // kRescaleThreshold unless overridden
   const uint32_t* v_amax;  // kFp8: per-head max |V| (f32 bits); O is scaled by amax / 448 in the epilogue
-  int debug_mode;  // measurement only (env SVG2_DEBUG_MODE): 1 = softmax skips max/exp (P = 0), 2 = cycle trace
 };
-
-// Cycle trace of the first item of CTA 0 (SVG2_DEBUG_MODE=2 with the SVG2_TRACE_PRINT build only; the product
-// build compiles no trace code): clock64 per tile and event, printed at kernel exit.  Events: 0/2 MMA a/b saw P,
-// 1/3 MMA a/b finished issuing PV+S, 4/6 softmax a/b got S, 5/7 softmax a/b handed P over, 8/9 producer issued K/V,
-// 10/11 softmax a/b has S in registers, 12/13 softmax a/b has the max (and any rescale), 14/15 softmax a/b issued
-// all P stores.
-constexpr int kTraceTiles = 48, kTraceEvents = 16;
-#ifdef SVG2_TRACE_PRINT
-#define TRACE(ev, t)                                                                                      \
-  do {                                                                                                    \
-    if (p.debug_mode == 2 && blockIdx.x == 0 && n_done == 0 && (t) < kTraceTiles && (threadIdx.x & 31) == 0) \
-      trace_buf[(ev)*kTraceTiles + (t)] = clock64();                                                      \
-  } while (0)
-#else
-#define TRACE(ev, t) \
-  do {               \
-  } while (0)
-#endif
-#define TRACE_MMA(ev, t) TRACE(ev, t)
 
 // Loads one 16-group tile of the item's key stream into a K or V stage.  Lanes 0..ngt-1 hold one group each; a
 // lane whose group does not continue the previous lane's full group starts a run segment and issues power-of-two
@@ -144,8 +116,7 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
 }
 
 // kPoly: in every 16-pair chunk of a row's 128 exponentials, kPoly pairs take 2^x on the FMA/ALU pipes (ex2_poly2)
-// instead of MUFU, which otherwise bounds the softmax (16 ex2/clk/SM; tools/xu_micro.cu).  Env SVG2_EXP_POLY
-// (0, 2, 4, 6, 8, 10) selects the split for measurements.
+// instead of MUFU, which otherwise bounds the softmax (16 ex2/clk/SM; tools/xu_micro.cu).
 // kFp8: the FP8 PV path (DESIGN R26) — V' arrives in e4m3 (scale 448 / amax per head), P is packed to e4m3 in
 // TMEM and PV runs as kind::f8f6f4 MMAs (K = 32 keys each, half the instructions of bf16); d = 128 only.
 template <int D, int kPoly, bool kFp8 = false>
@@ -163,13 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_slot;
   __shared__ int4 item_slot[2];
   __shared__ float2 merge_ml[kQTile];  // split items: (m, l) of warpgroup b's rows
-#ifdef SVG2_TRACE_PRINT
-  __shared__ long long trace_buf[kTraceEvents * kTraceTiles];
-  __shared__ int trace_T;
-#endif
 
   const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  int n_done = 0;  // items finished by this role (the trace covers the first one)
   if (warp == kWarpProducer && lane == 0) {
     tma_prefetch_desc(&mapQ);
     mbar_init(&bars.q_full, 1);
@@ -247,22 +213,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive_expect_tx(&bars.k_full[ks], bytes);
           __syncwarp();
           load_kv_tile<D>(kv.k, sK + ks * C::kTileBytes, &bars.k_full[ks], ngt, lane, gw);
-          TRACE(8, t);
           mbar_wait(&bars.v_empty[ks], kph ^ 1, 3);
           if (lane == 0) mbar_arrive_expect_tx(&bars.v_full[ks], kFp8 ? uint32_t(ngt) * 8u * D : bytes);
           __syncwarp();
           load_kv_tile<D>(kv.v, sV + ks * kVTile, &bars.v_full[ks], ngt, lane, gw, kFp8 ? 1 : C::kBlocks);
-          TRACE(9, t);
           gw = gw_next;
           if (++ks == kSt) {
             ks = 0;
             kph ^= 1;
           }
         }
-#ifdef SVG2_TRACE_PRINT
-        if (n_done == 0 && blockIdx.x == 0 && lane == 0) trace_T = T;
-#endif
-        ++n_done;
       }
     } else if (warp == kWarpMma) {
       // ============================ MMA issuer ============================
@@ -365,7 +325,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               vph ^= 1;
             }
           }
-          ++n_done;
           continue;
         }
         // prologue: S(0)
@@ -392,7 +351,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (g == 1 && !has_b) break;
             mbar_wait_warp(&bars.p_full[g], pph[g]);
             pph[g] ^= 1;
-            TRACE_MMA(2 * g, t);
             if (t == 0) {
               mbar_wait_warp(&bars.o_empty[g], oeph[g] ^ 1);
               oeph[g] ^= 1;
@@ -405,7 +363,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               mma_commit_warp(&bars.o_full[g]);
             }
-            TRACE_MMA(2 * g + 1, t);
           }
           mma_commit_warp(&bars.v_empty[vs]);
           if (more) {
@@ -421,7 +378,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             kph ^= 1;
           }
         }
-        ++n_done;
       }
     }
   } else {
@@ -458,7 +414,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t + t_step < T) word_next = __ldg(tw + t + t_step);
         mbar_wait(&bars.s_full[g], sph, 12 + g);
         sph ^= 1;
-        if ((warp & 3) == 0) TRACE(4 + 2 * g, t);
         tc_fence_after();
         uint32_t s0[32], s1[32], s2[32], s3[32];
         const bool full = word == kFullTileWord;
@@ -480,23 +435,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tS + 64, s2);
         tmem_ld32(tS + 96, s3);
         tmem_wait_ld();
-        if ((warp & 3) == 0) TRACE(10 + g, t);
-        if (p.debug_mode == 1) {  // measurement: the MMA/TMA pipeline without the softmax math
-          uint32_t z[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) z[e] = s0[e] & 0u;
-          tmem_st16(tS + 0, z);
-          tmem_st16(tS + 16, z);
-          tmem_st16(tS + 32, z);
-          tmem_st16(tS + 48, z);
-          l = 1.f;
-          m_used = 0.f;
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars.p_full[g]);
-          continue;
-        }
         // row max on the raw scores (scale > 0 preserves order); only tiles with padding rows need the mask
         if (!full) {
           apply_mask(s0, 0);
@@ -515,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mt = fmaxf(mx0, mx1) * sl2;
         if (t == t_first) {
           m_used = mt;
-        } else if (__any_sync(0xffffffffu, rloc < nrows && mt > m_used + p.rescale_thr)) {
+        } else if (__any_sync(0xffffffffu, rloc < nrows && mt > m_used + kRescaleThreshold)) {
           // only rows of the cluster vote: the tile's padding rows hold whatever follows the cluster in Q'
           // (another cluster or head), and must not change how the cluster's rows are rounded
           // warp-uniform branch (tcgen05.ld/st are .sync.aligned); rows whose max did not grow get alpha = 1
@@ -533,7 +471,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_used = m_new;
         }
-        if ((warp & 3) == 0) TRACE(12 + g, t);
         // p = 2^(s * scale*log2e - m): FFMA2 on pairs, MUFU ex2 per element, FADD2 row sums, bf16x2 packs
         const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m_used, -m_used);
         uint64_t lsum2 = f2(0.f, 0.f);
@@ -568,12 +505,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         exp_store(s1, 1);
         exp_store(s2, 2);
         exp_store(s3, 3);
-        if ((warp & 3) == 0) TRACE(14 + g, t);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.p_full[g]);
-        if ((warp & 3) == 0) TRACE(5 + 2 * g, t);
         float ls0, ls1;
         f2_split(lsum2, ls0, ls1);
         l += ls0 + ls1;
@@ -590,7 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (g == 1) merge_ml[rloc] = make_float2(m_used, l);
         named_bar_sync(1, 256);
         if (g == 1) {
-          ++n_done;
           continue;
         }
         const float2 mlb = merge_ml[rloc];
@@ -629,7 +563,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&bars.o_empty[0]);
           mbar_arrive(&bars.o_empty[1]);
         }
-        ++n_done;
         continue;
       }
       const float inv_l = (kFp8 ? __uint_as_float(__ldg(p.v_amax + (it.w & kItemBhMask))) * (1.f / 448.f) : 1.f) / l;
@@ -661,39 +594,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_empty[g]);
-      ++n_done;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == kWarpTmem) tmem_dealloc<512>(tmem);
-#ifdef SVG2_TRACE_PRINT
-  if (p.debug_mode == 2 && blockIdx.x == 0 && threadIdx.x == 0) {
-    const long long t0 = trace_buf[8 * kTraceTiles];
-    printf("svg2 trace: T=%d (cycles relative to the first K issue)\n", trace_T);
-    for (int t = 0; t < min(trace_T, kTraceTiles); ++t) {
-      printf("svg2 trace t=%2d", t);
-      for (int e = 0; e < kTraceEvents; ++e) printf(" %8lld", trace_buf[e * kTraceTiles + t] - t0);
-      printf("\n");
-    }
-  }
-#endif
 }
 
-template <int D>
-cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
-                     const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s,
-                     const uint32_t* v_amax = nullptr) {
-  const bool fp8 = v_amax != nullptr;
-  if (fp8 && D != 128) return cudaErrorNotSupported;
+cudaError_t run_attn_fp8(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
+                         const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s, const uint32_t* v_amax) {
+  constexpr int D = 128;
   CUtensorMap mq;
   KVMaps kv;
   if (!make_tmap_bf16(&mq, Qp, uint64_t(BH) * Nq, D, 128)) return cudaErrorInvalidValue;
-  for (int k = 0; k < kBoxKinds; ++k) {
-    const bool okv = fp8 ? make_tmap_u8(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k)
-                         : make_tmap_bf16(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k);
-    if (!make_tmap_bf16(&kv.k[k], Kp, uint64_t(BH) * Nk, D, 8u << k) || !okv) return cudaErrorInvalidValue;
-  }
+  for (int k = 0; k < kBoxKinds; ++k)
+    if (!make_tmap_bf16(&kv.k[k], Kp, uint64_t(BH) * Nk, D, 8u << k) ||
+        !make_tmap_u8(&kv.v[k], Vp, uint64_t(BH) * Nk, D, 8u << k))
+      return cudaErrorInvalidValue;
   Params p;
   p.items = ws.items;
   p.n_items = ws.n_items;
@@ -707,54 +624,23 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
   p.lse = lse;
   p.Nq = Nq;
   p.scale_log2 = scale * 1.4426950408889634f;
-  static const int debug_mode = [] {
-    const char* e = getenv("SVG2_DEBUG_MODE");
-    return e ? atoi(e) : 0;
-  }();
-  p.debug_mode = debug_mode;
-  static const float rescale_thr = [] {
-    const char* e = getenv("SVG2_RESCALE_LOG2");
-    return e ? float(atof(e)) : kRescaleThreshold;
-  }();
-  p.rescale_thr = rescale_thr;
   p.v_amax = v_amax;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static const int poly = [] {
-    const char* e = getenv("SVG2_EXP_POLY");
-    return e ? atoi(e) : kDefaultPoly;
-  }();
-  auto launch = [&](auto kernel, uint32_t smem = Cfg<D>::kSmemBytes) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kernel<<<sms, kThreads, smem, s>>>(mq, kv, p);
-  };
-  if constexpr (D == 128) {
-    if (fp8) {
-      if (poly == 2) launch(k_varblock_attn<D, 2, true>, Cfg<D>::kSmemBytesFp8);
-      else if (poly == 6) launch(k_varblock_attn<D, 6, true>, Cfg<D>::kSmemBytesFp8);
-      else launch(k_varblock_attn<D, kDefaultPoly, true>, Cfg<D>::kSmemBytesFp8);
-      return cudaGetLastError();
-    }
-  }
-  if (poly == 2) launch(k_varblock_attn<D, 2>);
-  else if (poly == 4) launch(k_varblock_attn<D, 4>);
-  else if (poly == 6) launch(k_varblock_attn<D, 6>);
-  else if (poly == 8) launch(k_varblock_attn<D, 8>);
-  else if (poly == 10) launch(k_varblock_attn<D, 10>);
-  else launch(k_varblock_attn<D, 0>);
+  auto kernel = k_varblock_attn<D, kDefaultPoly, true>;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg<D>::kSmemBytesFp8));
+  kernel<<<sms, kThreads, Cfg<D>::kSmemBytesFp8, s>>>(mq, kv, p);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_varblock_attention_v2(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
-                                      int Cq, int Ck, float scale, const int32_t* q_perm, void* O, float* lse,
-                                      AttnWs ws, cudaStream_t s, const uint32_t* v_amax) {
-  (void)Cq;
-  (void)Ck;
-  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s, v_amax);
-  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s, v_amax);
+cudaError_t launch_varblock_attention_fp8(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk,
+                                          int d, float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
+                                          cudaStream_t s, const uint32_t* v_amax) {
+  if (d != 128 || !v_amax) return cudaErrorNotSupported;
+  return run_attn_fp8(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s, v_amax);
 }
 
 }  // namespace svg2

@@ -12,7 +12,6 @@
 //                      Sums of bf16 values in fp64 are exact at these magnitudes, so the update is order-free and
 //                      bit-identical to the oracle's sequential sum.
 #include <cuda_bf16.h>
-#include <cstdlib>
 #include <type_traits>
 #include "internal.h"
 #include "ptx.cuh"
@@ -361,10 +360,12 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   }
   int j = lo, next = __ldg(off + j + 1) - p0;  // positions relative to p0
   asm volatile("cp.async.wait_all;" ::: "memory");
+  // every lane's cp.async writes into shared memory are made visible to the async proxy (the bulk store below) by
+  // that lane's own proxy fence before the warp barrier
+  if (kGather) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if (kGather) {  // X' (and Y') rows p0 .. p0 + nrow - 1 are contiguous: one bulk store each, issued by lane 0
     if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       uint8_t* gx = reinterpret_cast<uint8_t*>(Xp) + (size_t(bh) * N + p0) * kRowBytes;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gx), "r"(smem_u32(sx)),
                    "r"(nrow * kRowBytes)
@@ -431,15 +432,6 @@ __global__ void k_init_cold(const __nv_bfloat16* __restrict__ X, int N, int C, f
   cent[(size_t(bh) * C + j) * D + threadIdx.x] = __bfloat162float(X[(size_t(bh) * N + src) * D + threadIdx.x]);
 }
 
-// env SVG2_UPDATE_ASYNC=0: the register-staged kernel for the gather pass too (measurement)
-bool update_async() {
-  static const bool on = [] {
-    const char* e = getenv("SVG2_UPDATE_ASYNC");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
 template <int D>
 cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, const KmeansInit& init,
                        float* cent, int32_t* labels,
@@ -475,7 +467,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
     // the gather pass (last iteration) uses the asynchronous-copy kernel: K' + V' 0.69 -> 0.48 ms, Q' equal; the
     // plain update keeps the register-staged one (0.20 ms vs 0.33 ms: its accumulation phase has no loads in flight)
     if (it + 1 == iters && g.wait_y) cudaStreamWaitEvent(s, g.wait_y, 0);
-    if (update_async() && it + 1 == iters && g.Xp) {
+    if (it + 1 == iters && g.Xp) {
       constexpr int rows = kAsyncRows<true>;
       const dim3 grid_a((N + rows * kAsyncWarps - 1) / (rows * kAsyncWarps), BH);
       const size_t sm = size_t(kAsyncWarps) * 2 * rows * D * 2;
@@ -483,14 +475,10 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
       k_update_sum_async<D, true><<<grid_a, 32 * kAsyncWarps, sm, s>>>(
           X, N, C, perm, offsets, ws.c_sum, static_cast<__nv_bfloat16*>(g.Xp), static_cast<const __nv_bfloat16*>(g.Y),
           static_cast<__nv_bfloat16*>(g.Yp));
-    } else if (it + 1 == iters && g.Xp)
-      k_update_sum<D, true><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, ws.c_sum,
-                                                                 static_cast<__nv_bfloat16*>(g.Xp),
-                                                                 static_cast<const __nv_bfloat16*>(g.Y),
-                                                                 static_cast<__nv_bfloat16*>(g.Yp));
-    else
+    } else {
       k_update_sum<D, false><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, ws.c_sum, nullptr, nullptr,
                                                                   nullptr);
+    }
     k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, offsets, ws.c_sum, cent);
   }
   return cudaGetLastError();

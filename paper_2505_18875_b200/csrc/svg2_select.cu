@@ -235,11 +235,8 @@ cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* 
   int R = kRows;
   while (R > 1 && smem_of(R) > 200 * 1024) --R;
   const size_t smem = smem_of(R);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  // per launch (the attribute is per device; a process-wide flag would miss a second GPU and race across threads)
+  cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (pairs) cudaMemsetAsync(pairs, 0, size_t(BH) * sizeof(int64_t), s);
   k_select<<<dim3((Cq + R - 1) / R, BH), kSelThreads, smem, s>>>(cq, ck, sq, sk, Cq, Ck, d, double(scale), top_p,
                                                                   sortN, R, mask,
