@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SVG2_ABI_VERSION 2
+#define SVG2_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define SVG2_API __attribute__((visibility("default")))
@@ -88,6 +88,8 @@ typedef struct {
   int32_t *q_labels, *k_labels, *q_perm, *k_perm, *q_offsets, *k_offsets;
   uint8_t* mask;
   void* events[8];
+  double *q_objective, *k_objective; /* NULL or [iters, B, H, 2]: the Lloyd objective of each role per iteration,
+                                        as svg2_kmeans' `objective` (an extra launch per iteration when set) */
 } svg2_debug_t;
 
 SVG2_API const char* svg2_status_string(svg2_status_t status);
@@ -115,10 +117,16 @@ SVG2_API size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dims, const 
  * Cold start: strided rows, or k-means++ (flags & SVG2_INIT_KMEANSPP) with generator key (seed, 2*(b*H+h) + role),
  * role 0 for queries, 1 for keys (R25).
  * labels [B,H,N] out (last assign).  sizes [B,H,C] out.  perm / offsets: optional (NULL) outputs = the stable
- * permutation of the final labels, identical to what svg2_permute would compute. */
+ * permutation of the final labels, identical to what svg2_permute would compute.
+ * objective: optional (NULL) output [iters, B, H, 2] fp64, the Lloyd objective J = sum_n ||x_n - c_{label_n}||^2
+ * of iteration t: [t,b,h,0] = J_assign(t) with the centroids the assign step used, [t,b,h,1] =
+ * J_post(t) with the updated (f32) centroids, so J_assign(t) >= J_post(t) >= J_assign(t+1) up to rounding and
+ * near-ties.  Evaluated per cluster as sum ||x||^2 - 2 c.S + n ||c||^2 in fp64 (S = the cluster's fp64 sum).
+ * The centroid sums are a fixed-order segmented reduction: results are deterministic for any input. */
 SVG2_API svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C, int32_t iters,
-                          uint32_t flags, uint32_t seed, int32_t role, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
-                          int32_t* offsets, void* ws, size_t ws_bytes, void* stream);
+                                   uint32_t flags, uint32_t seed, int32_t role, float* centroids, int32_t* labels,
+                                   int32_t* sizes, int32_t* perm, int32_t* offsets, double* objective, void* ws,
+                                   size_t ws_bytes, void* stream);
 
 /* ---- A3, A4, A6: semantic-aware permutation.
  * Stable counting sort of the tokens by (label, index): perm [B,H,N] and offsets [B,H,C+1] out.  Then gathers

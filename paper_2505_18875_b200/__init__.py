@@ -52,7 +52,8 @@ class Config(ctypes.Structure):
 class Debug(ctypes.Structure):
     _fields_ = [("q_labels", ctypes.c_void_p), ("k_labels", ctypes.c_void_p), ("q_perm", ctypes.c_void_p),
                 ("k_perm", ctypes.c_void_p), ("q_offsets", ctypes.c_void_p), ("k_offsets", ctypes.c_void_p),
-                ("mask", ctypes.c_void_p), ("events", ctypes.c_void_p * 8)]
+                ("mask", ctypes.c_void_p), ("events", ctypes.c_void_p * 8), ("q_objective", ctypes.c_void_p),
+                ("k_objective", ctypes.c_void_p)]
 
 
 _lib = None
@@ -73,7 +74,7 @@ def load_library(path: str = LIB_PATH):
     lib.svg2_abi_version.restype = ctypes.c_int
     lib.svg2_workspace_size.argtypes = [ctypes.c_int, Dims, ctypes.POINTER(Config)]
     lib.svg2_workspace_size.restype = sz
-    lib.svg2_kmeans.argtypes = [vp, i32, i32, i32, i32, i32, i32, u32, u32, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    lib.svg2_kmeans.argtypes = [vp, i32, i32, i32, i32, i32, i32, u32, u32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_permute.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_select_topp.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, ctypes.c_float, ctypes.c_double, vp,
                                      vp, vp]
@@ -150,11 +151,12 @@ def _cold_flags(init: str) -> int:
 
 
 def kmeans(X: torch.Tensor, C: int, iters: int, centroids: torch.Tensor | None = None, return_perm: bool = False,
-           init: str = "strided", seed: int = 0, role: int = 0):
+           init: str = "strided", seed: int = 0, role: int = 0, return_objective: bool = False):
     """Lloyd k-means per (b,h) of X [B,H,N,d] bf16.  Warm start iff `centroids` ([B,H,C,d] f32) is given; it is
     updated in place.  Cold start: init="strided" (rows floor(jN/C), R2) or "kmeans++" with the
     generator key (seed, 2*(b*H+h) + role), role 0 = queries, 1 = keys (R25).
-    Returns (labels, sizes, centroids[, perm, offsets])."""
+    Returns (labels, sizes, centroids[, perm, offsets][, objective]); objective [iters, B, H, 2] f64 =
+    (J_assign, J_post) per iteration."""
     lib = load_library()
     _need(X, torch.bfloat16, "X", 4)
     B, H, N, d = X.shape
@@ -167,15 +169,16 @@ def kmeans(X: torch.Tensor, C: int, iters: int, centroids: torch.Tensor | None =
     sizes = torch.empty(B, H, C, dtype=torch.int32, device=X.device)
     perm = torch.empty(B, H, N, dtype=torch.int32, device=X.device) if return_perm else None
     offsets = torch.empty(B, H, C + 1, dtype=torch.int32, device=X.device) if return_perm else None
+    objective = torch.empty(iters, B, H, 2, dtype=torch.float64, device=X.device) if return_objective else None
     nbytes = workspace_size(ENTRY_KMEANS, B, H, N, N, d, C, iters=iters)
     ws = _workspace(max(nbytes, 256), X.device)
     flags = SVG2_WARM_START if warm else _cold_flags(init)
     _check("svg2_kmeans", lib.svg2_kmeans(_p(X), B, H, N, d, C, iters, flags, seed, role, _p(centroids),
-                                          _p(labels), _p(sizes), _p(perm), _p(offsets), _p(ws), ws.numel(),
-                                          _stream()))
-    if return_perm:
-        return labels, sizes, centroids, perm, offsets
-    return labels, sizes, centroids
+                                          _p(labels), _p(sizes), _p(perm), _p(offsets), _p(objective), _p(ws),
+                                          ws.numel(), _stream()))
+    out = (labels, sizes, centroids) + ((perm, offsets) if return_perm else ()) + \
+        ((objective,) if return_objective else ())
+    return out
 
 
 def permute(labels: torch.Tensor, C: int, X0: torch.Tensor | None = None, X1: torch.Tensor | None = None,
@@ -301,8 +304,11 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
                 k_perm=torch.empty(B, H, Nk, dtype=torch.int32, device=dev),
                 q_offsets=torch.empty(B, H, Cq + 1, dtype=torch.int32, device=dev),
                 k_offsets=torch.empty(B, H, Ck + 1, dtype=torch.int32, device=dev),
-                mask=torch.empty(B, H, Cq, Ck, dtype=torch.uint8, device=dev))
-            for name in ("q_labels", "k_labels", "q_perm", "k_perm", "q_offsets", "k_offsets", "mask"):
+                mask=torch.empty(B, H, Cq, Ck, dtype=torch.uint8, device=dev),
+                q_objective=torch.empty(iters, B, H, 2, dtype=torch.float64, device=dev),
+                k_objective=torch.empty(iters, B, H, 2, dtype=torch.float64, device=dev))
+            for name in ("q_labels", "k_labels", "q_perm", "k_perm", "q_offsets", "k_offsets", "mask", "q_objective",
+                         "k_objective"):
                 setattr(dbg, name, extras[name].data_ptr())
         if events is not None:
             for i, ev in enumerate(events[:8]):
@@ -374,6 +380,7 @@ class SVG2Attention:
         self.q_centroids = None
         self.k_centroids = None
         self.last_pairs = None
+        self.last_nq_nk = None
 
     def reset(self):
         self.q_centroids = self.k_centroids = None
@@ -388,11 +395,14 @@ class SVG2Attention:
                                         warm=warm, scale=self.scale, out=out)
         self.q_centroids, self.k_centroids = ex["q_centroids"], ex["k_centroids"]
         self.last_pairs = pairs
+        self.last_nq_nk = N * K.shape[2]
         return O
 
     def density(self) -> torch.Tensor:
         """selected pairs / (Nq Nk) per (b,h) of the last call."""
-        return self.last_pairs
+        if self.last_pairs is None:
+            raise RuntimeError("density(): no call yet")
+        return self.last_pairs.double() / self.last_nq_nk
 
 
 def default_scale(d: int) -> float:

@@ -54,9 +54,14 @@ struct KmeansWs {
   uint16_t* c_hi;     // [BH, Cpad, d] bf16 hi part of the centroids (assign operand)
   uint16_t* c_lo;     // [BH, Cpad, d] bf16 lo part: c - hi
   float* c_norm;      // [BH, Cpad]  ||c||^2 (f32), +inf for padding centroids
-  double* c_sum;      // [BH, C, d]  fp64 cluster sums of the update (kept zero between iterations)
+  double* c_sum;      // [BH, C, d]  fp64 sums of the clusters that lie inside one update chunk
+  double* c_part;     // [BH, ceil(N/kUpdMinRows), 2, d]  fp64 chunk partials of clusters crossing chunk boundaries
+  double* c_sq;       // [BH, C]  (objective) sum ||x||^2 per cluster, as c_sum
+  double* c_sqpart;   // [BH, ceil(N/kUpdMinRows), 2]
+  double* j_part;     // [BH, C, 2]  (objective) per-cluster J before / after the update
   void* pp;           // k-means++ seeding scratch (kmeanspp_ws_bytes)
 };
+constexpr int kUpdMinRows = 32;  // the smallest update chunk (rows per warp) of the segmented centroid reduction
 constexpr int kPPMaxBlocks = 64;  // k-means++: CTAs per head
 size_t kmeanspp_ws_bytes(int BH, int N);
 inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
@@ -68,6 +73,11 @@ inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   w.c_lo = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
   w.c_norm = c.take<float>(size_t(BH) * cent_pad(C));
   w.c_sum = c.take<double>(size_t(BH) * C * d);
+  const size_t nch = (size_t(N) + kUpdMinRows - 1) / kUpdMinRows;
+  w.c_part = c.take<double>(size_t(BH) * nch * 2 * d);
+  w.c_sq = c.take<double>(size_t(BH) * C);
+  w.c_sqpart = c.take<double>(size_t(BH) * nch * 2);
+  w.j_part = c.take<double>(size_t(BH) * C * 2);
   w.pp = c.take<uint8_t>(kmeanspp_ws_bytes(BH, N));
   return w;
 }
@@ -132,7 +142,7 @@ struct KmeansGather {
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
                           cudaStream_t s, int* launches, const KmeansInit& init = KmeansInit(),
-                          const KmeansGather& g = KmeansGather());
+                          const KmeansGather& g = KmeansGather(), double* objective = nullptr);
 cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH,
                                int Cq, int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
                                cudaStream_t s);
@@ -150,7 +160,7 @@ cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_off
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                       float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
                                       cudaStream_t s, const uint32_t* v_amax = nullptr);
-int kmeans_launch_count(int iters, bool warm);
+int kmeans_launch_count(int iters, bool warm, bool objective = false);
 cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
                             float* cent, void* ws, cudaStream_t s);
 int kmeanspp_launch_count(int BH, int N, int d);

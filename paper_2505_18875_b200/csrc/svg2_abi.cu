@@ -162,12 +162,12 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
     if (gk.Yp) gk.wait_y = arrive[2];
   }
   e = launch_kmeans(K, BH, dm.Nk, dm.d, cfg->Ck, cfg->iters, warm, k_centroids, w.lab_k, w.size_k, w.perm_k, w.off_k,
-                    w.km_k, sk, nullptr, init_k, gk);
+                    w.km_k, sk, nullptr, init_k, gk, dbg ? dbg->k_objective : nullptr);
   mark(1);  // with two streams: the fork point (stage "kmeans_k" then covers both roles)
   if (arrive) cudaStreamWaitEvent(s, arrive[0], 0);
   if (e == cudaSuccess)
     e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q,
-                      w.off_q, w.km_q, s, nullptr, init_q, gq);
+                      w.off_q, w.km_q, s, nullptr, init_q, gq, dbg ? dbg->q_objective : nullptr);
   if (s2) {  // join (always, so no work is left behind on s2 even after an error) and release (deferred by CUDA)
     cudaEventRecord(ev_join, s2);
     cudaStreamWaitEvent(s, ev_join, 0);
@@ -309,8 +309,9 @@ size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dm, const svg2_config
 }
 
 svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C, int32_t iters,
-                          uint32_t flags, uint32_t seed, int32_t role, float* centroids, int32_t* labels, int32_t* sizes, int32_t* perm,
-                          int32_t* offsets, void* ws, size_t ws_bytes, void* stream) {
+                          uint32_t flags, uint32_t seed, int32_t role, float* centroids, int32_t* labels,
+                          int32_t* sizes, int32_t* perm, int32_t* offsets, double* objective, void* ws,
+                          size_t ws_bytes, void* stream) {
   if (!X || !centroids || !labels || !sizes || (!ws && ws_bytes)) return SVG2_ERR_NULL_POINTER;
   svg2_status_t st = check_bhnd(B, H, N, d);
   if (st != SVG2_OK) return st;
@@ -330,7 +331,8 @@ svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_
   init.seed = seed;
   init.role = role;
   return from_cuda(launch_kmeans(X, B * H, N, d, C, iters, flags & SVG2_WARM_START, centroids, labels, sizes, perm,
-                                 offsets, kw, static_cast<cudaStream_t>(stream), nullptr, init));
+                                 offsets, kw, static_cast<cudaStream_t>(stream), nullptr, init, KmeansGather(),
+                                 objective));
 }
 
 svg2_status_t svg2_permute(const int32_t* labels, int32_t B, int32_t H, int32_t N, int32_t d, int32_t C,

@@ -9,8 +9,9 @@
 //                      centroid chunks are double-buffered in smem (TMA), accumulators four-deep in TMEM.
 //   stable sort of the labels (svg2_permute.cu)
 //   k_update         : c_j = (sum of its rows, fp64) / |cluster|, stored f32; empty clusters keep their centroid (R6).
-//                      Sums of bf16 values in fp64 are exact at these magnitudes, so the update is order-free and
-//                      bit-identical to the oracle's sequential sum.
+//                      A fixed-order segmented reduction (no atomics): deterministic for any data, and bit-identical
+//                      to the oracle's sequential sum whenever the fp64 sums of bf16 rows are exact.  Optionally the
+//                      Lloyd objective J before and after each update.
 #include <cuda_bf16.h>
 #include <type_traits>
 #include "internal.h"
@@ -209,29 +210,63 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-// Centroid update, pass 1: each warp sums a contiguous chunk of kSumRows permuted positions (rows gathered through
-// perm; lane l holds D/32 consecutive columns, so one row is one coalesced D*2-byte read) and flushes one fp64
-// partial per cluster the chunk touches with atomicAdd.  kSumUnroll rows are loaded before any is accumulated, so
-// each warp keeps several row reads in flight (the loop is latency-bound otherwise).  Sums of bf16 values in fp64
-// are exact at these magnitudes, so the result does not depend on the order of the atomics: deterministic and
-// bit-identical to a sequential fp64 sum.
-// On the last iteration the same pass also writes the permuted copy X' = pi X (A6) and optionally Y' = pi Y (V,
-// which shares pi_k), so the fused call reads Q and K once less (no separate gather launches).
+// Centroid update, pass 1 — a fixed-order segmented reduction.  The permuted positions [0, N) of a head are cut into
+// fixed chunks of R rows (R = the kernel's rows per warp); a warp sums its chunk's rows sequentially in fp64, one
+// partial per cluster segment.  A segment that is a whole cluster (the cluster lies inside the chunk) is stored as its
+// sum; a cluster that crosses chunk boundaries leaves one partial per chunk (slot 0 = the chunk's first segment, slot 1
+// = its last), and k_update_mean adds them in chunk order.  Plain stores, no atomics: the summation order is a function
+// of (offsets, R) alone, so the result is deterministic for any data (no reliance on fp64 sums of bf16 being exact),
+// and it is the oracle's sequential sum bit for bit whenever those sums are exact (sums of bf16 values whose exponent
+// spread + log2 |cluster| + 8 <= 53).  With `sq` set, the segment's sum of squared norms sum ||x||^2 (fp64, lane
+// partials reduced by a fixed shuffle tree) is stored the same way for the Lloyd objective.
+struct SegOut {
+  double* sum;     // [BH, C, D]       complete cluster sums
+  double* part;    // [BH, nch, 2, D]  partial segments of clusters crossing chunk boundaries
+  double* sq;      // [BH, C]          (objective) complete sum ||x||^2, or nullptr
+  double* sqpart;  // [BH, nch, 2]
+  int nch;         // chunks per head at this R
+};
+
+template <int D>
+__device__ __forceinline__ void store_segment(const SegOut& o, const int32_t* off, int bh, int C, int j, int chunk,
+                                              int p0, int p1, int lane, const double* acc, double sq) {
+  constexpr int kCols = D / 32;
+  const int o0 = __ldg(off + j), o1 = __ldg(off + j + 1);
+  double* dst;
+  double* dsq;
+  if (o0 >= p0 && o1 <= p1) {  // the whole cluster lies in this chunk
+    dst = o.sum + (size_t(bh) * C + j) * D;
+    dsq = o.sq ? o.sq + size_t(bh) * C + j : nullptr;
+  } else {
+    const size_t slot = (size_t(bh) * o.nch + chunk) * 2 + (o0 <= p0 ? 0 : 1);
+    dst = o.part + slot * D;
+    dsq = o.sq ? o.sqpart + slot : nullptr;
+  }
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) dst[kCols * lane + c] = acc[c];
+  if (dsq) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, s);
+    if (lane == 0) *dsq = sq;
+  }
+}
+
 constexpr int kSumRows = 64, kSumUnroll = 8, kSumWarps = 4;
 
-template <int D, bool kGather>
+// Plain update (no gather): rows gathered through perm into registers, kSumUnroll loads in flight per warp (lane l
+// holds D/32 consecutive columns, so one row is one coalesced D*2-byte read).
+template <int D>
 __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat16* __restrict__ X, int N, int C,
                                                              const int32_t* __restrict__ perm,
-                                                             const int32_t* __restrict__ offsets,
-                                                             double* __restrict__ sum, __nv_bfloat16* __restrict__ Xp,
-                                                             const __nv_bfloat16* __restrict__ Y,
-                                                             __nv_bfloat16* __restrict__ Yp) {
+                                                             const int32_t* __restrict__ offsets, SegOut out) {
   constexpr int kCols = D / 32;  // 4 (d = 128) or 2 (d = 64) bf16 per lane
   using Vec = typename std::conditional<kCols == 4, uint2, uint32_t>::type;
   const int bh = blockIdx.y, lane = threadIdx.x & 31;
-  const int p0 = (blockIdx.x * kSumWarps + (threadIdx.x >> 5)) * kSumRows;
+  const int chunk = blockIdx.x * kSumWarps + (threadIdx.x >> 5);
+  const int p0 = chunk * kSumRows;
   if (p0 >= N) return;
   const int p1 = min(N, p0 + kSumRows);
+  const bool want_sq = out.sq != nullptr;
   const int32_t* off = offsets + size_t(bh) * (C + 1);
   int lo = 0, hi = C - 1;  // cluster of position p0: last j with off[j] <= p0
   while (lo < hi) {
@@ -240,22 +275,16 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
   }
   int j = lo, next = __ldg(off + j + 1);
   const Vec* Xv = reinterpret_cast<const Vec*>(X) + size_t(bh) * N * 32;  // 32 Vec per row
-  Vec* Xpv = kGather ? reinterpret_cast<Vec*>(Xp) + size_t(bh) * N * 32 : nullptr;
-  const Vec* Yv = kGather && Y ? reinterpret_cast<const Vec*>(Y) + size_t(bh) * N * 32 : nullptr;
-  Vec* Ypv = kGather && Yp ? reinterpret_cast<Vec*>(Yp) + size_t(bh) * N * 32 : nullptr;
   const int32_t* pm = perm + size_t(bh) * N;
-  double* sb = sum + size_t(bh) * C * D;
-  double acc[kCols];
+  double acc[kCols], sq = 0.0;
 #pragma unroll
   for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
   bool any = false;
   auto flush = [&] {
-    if (any) {
-#pragma unroll
-      for (int c = 0; c < kCols; ++c) atomicAdd(sb + size_t(j) * D + kCols * lane + c, acc[c]);
-    }
+    if (any) store_segment<D>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
     for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+    sq = 0.0;
     any = false;
   };
   for (int pb = p0; pb < p1; pb += kSumUnroll) {
@@ -266,27 +295,11 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
       const int src = __shfl_sync(0xffffffffu, src_l, u);
       if (pb + u < p1) v[u] = __ldg(Xv + size_t(src) * 32 + lane);
     }
-    if (kGather) {
-      if (Ypv) {  // the gather-only tensor (V' = pi_k V): loads in flight together with X's
-        Vec y[kSumUnroll];
-#pragma unroll
-        for (int u = 0; u < kSumUnroll; ++u) {
-          const int src = __shfl_sync(0xffffffffu, src_l, u);
-          if (pb + u < p1) y[u] = __ldg(Yv + size_t(src) * 32 + lane);
-        }
-#pragma unroll
-        for (int u = 0; u < kSumUnroll; ++u)
-          if (pb + u < p1) Ypv[size_t(pb + u) * 32 + lane] = y[u];
-      }
-#pragma unroll
-      for (int u = 0; u < kSumUnroll; ++u)
-        if (pb + u < p1) Xpv[size_t(pb + u) * 32 + lane] = v[u];
-    }
 #pragma unroll
     for (int u = 0; u < kSumUnroll; ++u) {
       const int pos = pb + u;
       if (pos >= p1) break;
-      while (pos >= next) {  // crossed into the next cluster: flush the partial sum
+      while (pos >= next) {  // crossed into the next cluster: store the segment
         flush();
         ++j;
         next = __ldg(off + j + 1);
@@ -297,6 +310,7 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
         const float2 f = __bfloat1622float2(h[c]);
         acc[2 * c] += double(f.x);
         acc[2 * c + 1] += double(f.y);
+        if (want_sq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
       }
       any = true;
     }
@@ -308,30 +322,28 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
 // lane-instruction): a warp puts all kAsyncRows rows of its chunk (X and Y) in flight at once through shared memory
 // instead of kSumUnroll rows through registers, and the permuted copies leave shared memory as one bulk copy per
 // tensor (the chunk's rows are contiguous in X').  Measured (ncu, HunyuanVideo): K' + V' 0.69 -> 0.48 ms, Q' equal;
-// for the plain update the register-staged kernel stays faster (0.20 vs 0.33 ms).
-constexpr int kAsyncWarps = 4;
-template <bool kGather>
-constexpr int kAsyncRows = kGather ? 32 : 64;  // <= 64: two perm registers per lane
-template <int D, bool kGather>
+// for the plain update the register-staged kernel stays faster (0.20 vs 0.33 ms).  Same segmented reduction (R = 32).
+constexpr int kAsyncWarps = 4, kAsyncRows = kUpdMinRows;
+template <int D>
 __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
     const __nv_bfloat16* __restrict__ X, int N, int C, const int32_t* __restrict__ perm,
-    const int32_t* __restrict__ offsets, double* __restrict__ sum, __nv_bfloat16* __restrict__ Xp,
+    const int32_t* __restrict__ offsets, SegOut out, __nv_bfloat16* __restrict__ Xp,
     const __nv_bfloat16* __restrict__ Y, __nv_bfloat16* __restrict__ Yp) {
   constexpr int kCols = D / 32;           // bf16 per lane in the accumulation
   constexpr int kRowBytes = D * 2;        // 256 (d = 128) or 128 (d = 64)
   constexpr int kVecPerRow = kRowBytes / 16;
-  constexpr int kTensors = kGather ? 2 : 1;
-  constexpr int kRows = kAsyncRows<kGather>;  // rows per warp (the gather pass holds two tensors per row)
+  constexpr int kRows = kAsyncRows;
   extern __shared__ __align__(128) uint8_t sm_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, bh = blockIdx.y;
-  uint8_t* sx = sm_raw + size_t(warp) * kTensors * kRows * kRowBytes;  // [kRows][row] X rows of this warp
-  uint8_t* sy = sx + kRows * kRowBytes;                                 // [kRows][row] Y rows (kGather)
-  const int p0 = (blockIdx.x * kAsyncWarps + warp) * kRows;
+  uint8_t* sx = sm_raw + size_t(warp) * 2 * kRows * kRowBytes;  // [kRows][row] X rows of this warp
+  uint8_t* sy = sx + kRows * kRowBytes;                          // [kRows][row] Y rows
+  const int chunk = blockIdx.x * kAsyncWarps + warp;
+  const int p0 = chunk * kRows;
   if (p0 >= N) return;
   const int nrow = min(N - p0, kRows);
-  const bool with_y = kGather && Y != nullptr;
+  const bool with_y = Y != nullptr, want_sq = out.sq != nullptr;
   const int32_t* pm = perm + size_t(bh) * N + p0;
-  const int src0 = lane < nrow ? __ldg(pm + lane) : 0, src1 = kRows > 32 && lane + 32 < nrow ? __ldg(pm + 32 + lane) : 0;
+  const int src0 = lane < nrow ? __ldg(pm + lane) : 0;
   const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + size_t(bh) * N * kRowBytes;
   const uint8_t* yb = with_y ? reinterpret_cast<const uint8_t*>(Y) + size_t(bh) * N * kRowBytes : nullptr;
   // issue: 32 lanes cover 32 / kVecPerRow rows per step, one 16-byte piece each
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   const int piece = lane % kVecPerRow, rsub = lane / kVecPerRow;
   for (int r0 = 0; r0 < nrow; r0 += kRowsPerStep) {
     const int r = r0 + rsub;
-    const int src = __shfl_sync(0xffffffffu, r < 32 ? src0 : src1, r & 31);
+    const int src = __shfl_sync(0xffffffffu, src0, r & 31);
     if (r < nrow) {
       const uint32_t dst = smem_u32(sx + r * kRowBytes + piece * 16);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(xb + size_t(src) * kRowBytes + piece * 16)
@@ -362,36 +374,32 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   asm volatile("cp.async.wait_all;" ::: "memory");
   // every lane's cp.async writes into shared memory are made visible to the async proxy (the bulk store below) by
   // that lane's own proxy fence before the warp barrier
-  if (kGather) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
-  if (kGather) {  // X' (and Y') rows p0 .. p0 + nrow - 1 are contiguous: one bulk store each, issued by lane 0
-    if (lane == 0) {
-      uint8_t* gx = reinterpret_cast<uint8_t*>(Xp) + (size_t(bh) * N + p0) * kRowBytes;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gx), "r"(smem_u32(sx)),
+  if (lane == 0) {  // X' (and Y') rows p0 .. p0 + nrow - 1 are contiguous: one bulk store each
+    uint8_t* gx = reinterpret_cast<uint8_t*>(Xp) + (size_t(bh) * N + p0) * kRowBytes;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gx), "r"(smem_u32(sx)),
+                 "r"(nrow * kRowBytes)
+                 : "memory");
+    if (with_y) {
+      uint8_t* gy = reinterpret_cast<uint8_t*>(Yp) + (size_t(bh) * N + p0) * kRowBytes;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gy), "r"(smem_u32(sy)),
                    "r"(nrow * kRowBytes)
                    : "memory");
-      if (with_y) {
-        uint8_t* gy = reinterpret_cast<uint8_t*>(Yp) + (size_t(bh) * N + p0) * kRowBytes;
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gy), "r"(smem_u32(sy)),
-                     "r"(nrow * kRowBytes)
-                     : "memory");
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
-  double* sb = sum + size_t(bh) * C * D;
-  double acc[kCols];
+  double acc[kCols], sq = 0.0;
 #pragma unroll
   for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
   bool any = false;
+  const int p1 = p0 + nrow;
   for (int r = 0; r < nrow; ++r) {
-    while (r >= next) {  // crossed into the next cluster: flush the partial sum
-      if (any) {
-#pragma unroll
-        for (int c = 0; c < kCols; ++c) atomicAdd(sb + size_t(j) * D + kCols * lane + c, acc[c]);
-      }
+    while (r >= next) {  // crossed into the next cluster: store the segment
+      if (any) store_segment<D>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+      sq = 0.0;
       any = false;
       ++j;
       next = __ldg(off + j + 1) - p0;
@@ -402,27 +410,87 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
       const float2 f = __bfloat1622float2(h[c]);
       acc[2 * c] += double(f.x);
       acc[2 * c + 1] += double(f.y);
+      if (want_sq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
     }
     any = true;
   }
-  if (any) {
-#pragma unroll
-    for (int c = 0; c < kCols; ++c) atomicAdd(sb + size_t(j) * D + kCols * lane + c, acc[c]);
-  }
-  if (kGather && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live
+  if (any) store_segment<D>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live
   __syncwarp();
 }
 
-// Pass 2: c_j = sum_j / |cluster j| (fp64, rounded to f32); empty clusters keep their centroid (R6).  The sums are
-// zeroed for the next iteration.
+// Pass 2: S_j = the cluster's sum (complete, or its chunk partials added in chunk order), c_j = S_j / |cluster j|
+// (fp64, rounded to f32); empty clusters keep their centroid (R6).  With `jpart`, the cluster's share of the Lloyd
+// objective before and after the update:
+//   J_assign_j = sum ||x||^2 - 2 c_old . S_j + n ||c_old||^2,   J_post_j = the same with the new (f32) centroid,
+// reduced over the D columns by a fixed tree (deterministic); empty clusters contribute 0.
 template <int D>
-__global__ void __launch_bounds__(D) k_update_mean(int C, const int32_t* __restrict__ offsets,
-                                                   double* __restrict__ sum, float* __restrict__ cent) {
+__global__ void __launch_bounds__(D) k_update_mean(int C, int R, const int32_t* __restrict__ offsets, SegOut in,
+                                                   float* __restrict__ cent, double* __restrict__ jpart) {
   const int j = blockIdx.x, bh = blockIdx.y, k = threadIdx.x;
-  const int cnt = offsets[size_t(bh) * (C + 1) + j + 1] - offsets[size_t(bh) * (C + 1) + j];
-  double* s = sum + (size_t(bh) * C + j) * D + k;
-  if (cnt > 0) cent[(size_t(bh) * C + j) * D + k] = float(*s / double(cnt));
-  *s = 0.0;
+  const int o0 = offsets[size_t(bh) * (C + 1) + j], o1 = offsets[size_t(bh) * (C + 1) + j + 1];
+  const int cnt = o1 - o0;
+  if (cnt == 0) {
+    if (jpart && k == 0) jpart[(size_t(bh) * C + j) * 2] = jpart[(size_t(bh) * C + j) * 2 + 1] = 0.0;
+    return;
+  }
+  const int c0 = o0 / R, c1 = (o1 - 1) / R;
+  double s, sq = 0.0;
+  if (c0 == c1) {
+    s = in.sum[(size_t(bh) * C + j) * D + k];
+    if (jpart) sq = in.sq[size_t(bh) * C + j];
+  } else {
+    size_t slot = (size_t(bh) * in.nch + c0) * 2 + (o0 <= c0 * R ? 0 : 1);
+    s = in.part[slot * D + k];
+    if (jpart) sq = in.sqpart[slot];
+    for (int c = c0 + 1; c <= c1; ++c) {
+      slot = (size_t(bh) * in.nch + c) * 2;
+      s += in.part[slot * D + k];
+      if (jpart) sq += in.sqpart[slot];
+    }
+  }
+  float* cp = cent + (size_t(bh) * C + j) * D + k;
+  const double c_old = double(*cp);
+  const float c_new = float(s / double(cnt));
+  *cp = c_new;
+  if (jpart) {
+    __shared__ double red[2][D / 32];
+    double a = double(cnt) * c_old * c_old - 2.0 * c_old * s;
+    double b = double(cnt) * double(c_new) * double(c_new) - 2.0 * double(c_new) * s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((k & 31) == 0) {
+      red[0][k >> 5] = a;
+      red[1][k >> 5] = b;
+    }
+    __syncthreads();
+    if (k == 0) {
+      double ta = sq, tb = sq;
+      for (int w = 0; w < D / 32; ++w) {
+        ta += red[0][w];
+        tb += red[1][w];
+      }
+      jpart[(size_t(bh) * C + j) * 2] = ta;
+      jpart[(size_t(bh) * C + j) * 2 + 1] = tb;
+    }
+  }
+}
+
+// Pass 3 (objective requested only): J(t) of each head = sum over clusters in ascending j, objective[bh] =
+// (J_assign, J_post).
+__global__ void k_objective(int BH, int C, const double* __restrict__ jpart, double* __restrict__ objective) {
+  const int bh = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bh >= BH) return;
+  double a = 0.0, b = 0.0;
+  for (int j = 0; j < C; ++j) {
+    a += jpart[(size_t(bh) * C + j) * 2];
+    b += jpart[(size_t(bh) * C + j) * 2 + 1];
+  }
+  objective[size_t(bh) * 2] = a;
+  objective[size_t(bh) * 2 + 1] = b;
 }
 
 template <int D>
@@ -436,7 +504,7 @@ template <int D>
 cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, const KmeansInit& init,
                        float* cent, int32_t* labels,
                        int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws, cudaStream_t s,
-                       const KmeansGather& g) {
+                       const KmeansGather& g, double* objective) {
   const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(Xv);
   const int Cpad = cent_pad(C);
   CUtensorMap mx, mh, ml;
@@ -455,7 +523,6 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
   } else if (!warm) {
     k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
   }
-  cudaMemsetAsync(ws.c_sum, 0, size_t(BH) * C * D * sizeof(double), s);
   __nv_bfloat16* hi = reinterpret_cast<__nv_bfloat16*>(ws.c_hi);
   __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
   for (int it = 0; it < iters; ++it) {
@@ -463,23 +530,25 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
     k_assign_tc<D><<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
-    const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
     // the gather pass (last iteration) uses the asynchronous-copy kernel: K' + V' 0.69 -> 0.48 ms, Q' equal; the
     // plain update keeps the register-staged one (0.20 ms vs 0.33 ms: its accumulation phase has no loads in flight)
     if (it + 1 == iters && g.wait_y) cudaStreamWaitEvent(s, g.wait_y, 0);
-    if (it + 1 == iters && g.Xp) {
-      constexpr int rows = kAsyncRows<true>;
-      const dim3 grid_a((N + rows * kAsyncWarps - 1) / (rows * kAsyncWarps), BH);
-      const size_t sm = size_t(kAsyncWarps) * 2 * rows * D * 2;
-      cudaFuncSetAttribute(k_update_sum_async<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-      k_update_sum_async<D, true><<<grid_a, 32 * kAsyncWarps, sm, s>>>(
-          X, N, C, perm, offsets, ws.c_sum, static_cast<__nv_bfloat16*>(g.Xp), static_cast<const __nv_bfloat16*>(g.Y),
+    const bool gather = it + 1 == iters && g.Xp;
+    const int R = gather ? kAsyncRows : kSumRows;
+    SegOut seg{ws.c_sum, ws.c_part, objective ? ws.c_sq : nullptr, ws.c_sqpart, (N + R - 1) / R};
+    if (gather) {
+      const dim3 grid_a((N + kAsyncRows * kAsyncWarps - 1) / (kAsyncRows * kAsyncWarps), BH);
+      const size_t sm = size_t(kAsyncWarps) * 2 * kAsyncRows * D * 2;
+      cudaFuncSetAttribute(k_update_sum_async<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+      k_update_sum_async<D><<<grid_a, 32 * kAsyncWarps, sm, s>>>(
+          X, N, C, perm, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp), static_cast<const __nv_bfloat16*>(g.Y),
           static_cast<__nv_bfloat16*>(g.Yp));
     } else {
-      k_update_sum<D, false><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, ws.c_sum, nullptr, nullptr,
-                                                                  nullptr);
+      const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
+      k_update_sum<D><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, seg);
     }
-    k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, offsets, ws.c_sum, cent);
+    k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, R, offsets, seg, cent, objective ? ws.j_part : nullptr);
+    if (objective) k_objective<<<(BH + 127) / 128, 128, 0, s>>>(BH, C, ws.j_part, objective + size_t(it) * BH * 2);
   }
   return cudaGetLastError();
 }
@@ -487,20 +556,24 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
 }  // namespace
 
 // split + assign + sort (3) + sum + mean per iteration, plus the cold init
-int kmeans_launch_count(int iters, bool warm) { return (warm ? 0 : 1) + iters * (4 + kSortLaunches); }
+int kmeans_launch_count(int iters, bool warm, bool objective) {
+  return (warm ? 0 : 1) + iters * (4 + kSortLaunches + (objective ? 1 : 0));
+}
 
 cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
-                          cudaStream_t s, int* launches, const KmeansInit& init, const KmeansGather& g) {
+                          cudaStream_t s, int* launches, const KmeansInit& init, const KmeansGather& g,
+                          double* objective) {
   if (!perm) perm = ws.perm;
   if (!offsets) offsets = ws.offsets;
   if (launches) {
-    *launches += kmeans_launch_count(iters, warm);
+    *launches += kmeans_launch_count(iters, warm, objective != nullptr);
     if (!warm && init.kmeanspp) *launches += kmeanspp_launch_count(BH, N, d) - 1;  // replaces the strided init
   }
   if (d == 128)
-    return run_kmeans<128>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s, g);
-  return run_kmeans<64>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s, g);
+    return run_kmeans<128>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s, g,
+                           objective);
+  return run_kmeans<64>(X, BH, N, C, iters, warm, init, centroids, labels, sizes, perm, offsets, ws, s, g, objective);
 }
 
 }  // namespace svg2

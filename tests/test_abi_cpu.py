@@ -42,7 +42,7 @@ def test_binding_names_match_abi():
 
 
 def test_status_strings_and_version(lib):
-    assert lib.svg2_abi_version() == 2
+    assert lib.svg2_abi_version() == 3
     assert lib.svg2_status_string(0) == b"SVG2_OK"
     assert lib.svg2_status_string(5) == b"SVG2_ERR_WORKSPACE_TOO_SMALL"
 
@@ -90,8 +90,8 @@ def test_validation_rejects_before_touching_the_device(lib):
     assert lib.svg2_sparse_attention(fake, fake, fake, dims, ctypes.byref(cfg_fp8), fake, fake, fake, None, None,
                                      fake, 1 << 30, None) == 3
     # svg2_kmeans: role must be 0 (queries) or 1 (keys)
-    assert lib.svg2_kmeans(fake, 1, 1, 256, 64, 8, 1, m.SVG2_INIT_KMEANSPP, 7, 2, fake, fake, fake, None, None, fake,
-                           1 << 30, None) == 3
+    assert lib.svg2_kmeans(fake, 1, 1, 256, 64, 8, 1, m.SVG2_INIT_KMEANSPP, 7, 2, fake, fake, fake, None, None, None,
+                           fake, 1 << 30, None) == 3
     # d unsupported -> SVG2_ERR_INVALID_SHAPE
     assert lib.svg2_sparse_attention(fake, fake, fake, m.Dims(1, 1, 256, 256, 80), ctypes.byref(cfg), fake, fake,
                                      fake, None, None, fake, 1 << 30, None) == 2

@@ -76,6 +76,66 @@ def test_kmeans_teacher_forced(svg2, oracle_mod, N, d, C):
     assert total_bad <= max(2, N // 1000)
 
 
+@pytest.mark.parametrize("N,d,C,iters", [(1024, 64, 16, 5), (5000, 128, 100, 3)])
+def test_kmeans_objective(svg2, oracle_mod, N, d, C, iters):
+    """The Lloyd objective the library reports per iteration: equal to the oracle's J_assign / J_post
+    (same labels: the cold strided run of both sides) within 1e-9 relative, and J_assign(t) >= J_post(t) >=
+    J_assign(t+1) on the GPU side within 1e-12 relative.  Also through the fused call's debug."""
+    q, k, _ = random_qkv(2, 2, N, N, d, seed=N + 3, groups=16)
+    X = to_dev(q)
+    labels, sizes, cent, obj = svg2.kmeans(X, C, iters, return_objective=True)
+    obj = obj.cpu().numpy()
+    assert obj.shape == (iters, 2, 2, 2)
+    for b in range(2):
+        for h in range(2):
+            ol, oc, osz, ja, jp = oracle_mod.kmeans(to_f64(X)[b, h], C, iters, return_objective=True)
+            # an R16 near-tie flip in an earlier iteration moves J by ~1e-5 of one row's distance: looser bound then
+            rtol = 1e-9 if np.array_equal(labels.cpu().numpy()[b, h], ol) else 1e-6
+            ga, gp = obj[:, b, h, 0], obj[:, b, h, 1]
+            np.testing.assert_allclose(ga, ja, rtol=rtol)
+            np.testing.assert_allclose(gp, jp, rtol=rtol)
+            for t in range(iters):
+                assert gp[t] <= ga[t] * (1 + 1e-12)
+                if t + 1 < iters:
+                    assert ga[t + 1] <= gp[t] * (1 + 1e-12)
+    Q, K = to_dev(q), to_dev(k)
+    _, _, ex = svg2.sparse_attention(Q, K, K, C, C, iters, 0.9, debug=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ex["q_objective"].cpu(), torch.from_numpy(obj))
+    _, _, _, kobj = svg2.kmeans(K, C, iters, return_objective=True)
+    assert torch.equal(ex["k_objective"], kobj)
+
+
+def test_kmeans_update_deterministic_wide_exponent_spread(svg2):
+    """Centroid sums whose fp64 accumulation is NOT exact (bf16 rows of magnitude 2^4 mixed with 2^-30 in one cluster:
+    exponent spread + mantissa + log2 |cluster| > 53 bits): the segmented update adds in a fixed order, so the result
+    is identical however the heads are batched or scheduled, and within one f32 ulp of the correctly rounded mean
+    (math.fsum)."""
+    import math as _m
+    rng = np.random.default_rng(99)
+    N, d = 6000, 64
+    x = rng.standard_normal((N, d)).astype(np.float32)
+    x[rng.random(N) < 0.5] *= np.float32(2.0 ** -30)
+    x[rng.random(N) < 0.3] *= np.float32(16.0)
+    bits = svg2_synth.f32_to_bf16_bits(x)
+    one = to_dev(bits.reshape(1, 1, N, d))
+    many = to_dev(np.broadcast_to(bits, (2, 3, N, d)).copy())
+    for C in (1, 3):
+        _, s1, c1 = svg2.kmeans(one, C, 2)
+        _, s2, c2 = svg2.kmeans(one, C, 2)
+        _, sm, cm = svg2.kmeans(many, C, 2)
+        assert torch.equal(c1, c2)
+        for b in range(2):
+            for h in range(3):
+                assert torch.equal(cm[b, h], c1[0, 0]) and torch.equal(sm[b, h], s1[0, 0])
+    labels, sizes, cent = svg2.kmeans(one, 1, 1)
+    X64 = to_f64(one)[0, 0]
+    exact = np.array([_m.fsum(X64[:, c]) / N for c in range(d)]).astype(np.float32)
+    got = cent.cpu().numpy()[0, 0, 0]
+    ulp = np.spacing(np.abs(exact))
+    assert np.all(np.abs(got.astype(np.float64) - exact.astype(np.float64)) <= ulp + 1e-12)
+
+
 def test_kmeans_cold_matches_oracle_tiny(svg2, oracle_mod):
     wl = svg2_synth.WORKLOADS["tiny"]
     q, k, _ = svg2_synth.generate(wl)
@@ -205,6 +265,27 @@ def test_varblock_attention_parity(svg2, oracle_mod, case):
             check_attention(O[b, h], ref, f"{case} b{b} h{h}")
             tok = m_h[b, h][lq_h[b, h]][:, lk_h[b, h]]
             assert int(pairs[b, h]) == int(tok.sum())
+
+
+@pytest.mark.parametrize("vscale,vshift", [(7.3, 0.0), (5.1, 6.5)])
+def test_attention_large_v(svg2, oracle_mod, vscale, vshift):
+    """|V| well above 1 (a wide N(shift, scale^2) V, rounded to bf16): the error of a bf16-output, fp32-accumulated
+    attention grows with the magnitude of V (bf16 P in PV: relative 2^-9 of sum p|v|; bf16 output: 2^-9 of |o|), so
+    the P5 tolerances are applied in units of max|V| / 4 (the max of an N(0,1) sample of this size is about 4)."""
+    q, k, _ = random_qkv(1, 2, 3001, 2900, 128, seed=71, groups=12)
+    rng = np.random.default_rng(72)
+    v = svg2_synth.f32_to_bf16_bits((vscale * rng.standard_normal((1, 2, 2900, 128)) + vshift).astype(np.float32))
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, 20, 40, 3, 0.9, debug=True)
+    Q64, K64, V64 = to_f64(Q), to_f64(K), to_f64(V)
+    unit = float(np.abs(V64).max()) / 4.0
+    assert unit > 4.0
+    for h in range(2):
+        lq, lk, m = (ex[n].cpu().numpy()[0, h] for n in ("q_labels", "k_labels", "mask"))
+        ref = oracle_mod.attention_rows(Q64[0, h], K64[0, h], V64[0, h], f32scale(128), lq=lq, lk=lk, mask=m)
+        err = np.abs(to_f64(O[0, h]) - ref)
+        assert err.max() <= MAX_ABS * unit and err.mean() <= MEAN_ABS * unit, \
+            f"head {h}: max {err.max():.3e} mean {err.mean():.3e} (unit {unit:.2f})"
 
 
 def test_varblock_lse(svg2, oracle_mod):
@@ -344,6 +425,11 @@ def test_warm_start_cache(svg2):
     O2 = attn(Q, K, V)  # converged cache: a warm step is (near) a fixed point
     assert (attn.q_centroids - cq).abs().max().item() < 1e-3
     assert (O1.float() - O2.float()).abs().max().item() < 5e-2
+    # density() is selected pairs / (Nq Nk) per (b,h) (include/svg2.h), a fraction, not the raw pair count
+    dens = attn.density()
+    assert dens.shape == (1, 2) and dens.dtype == torch.float64
+    assert torch.all((dens > 0) & (dens <= 1))
+    assert torch.equal(dens, attn.last_pairs.double() / (3000 * 3000))
 
 
 def test_abi_errors(svg2):
@@ -397,33 +483,73 @@ def test_abi_errors(svg2):
 # ------------------------------------------------------------------ full size, bench launch configuration
 @pytest.mark.parametrize("name", ["hunyuan720p", "wan720p"])
 def test_fullsize_sampled_rows(svg2, oracle_mod, name):
-    """BASELINE configs[1] and [2] at full size through the fused call (cold 5 iterations, then a warm 2-iteration call as
-    bench.py times it); the oracle checks sampled query rows of two heads, fed with the GPU's intermediates."""
+    """BASELINE configs[1] and [2] at full size, in the launch configuration bench.py times: a cold 5-iteration call
+    fills the centroid caches, then the warm 2-iteration fused call is checked stage by stage against the oracle
+    (protocol P2-P6) on one head per role (k-means, teacher-forced per iteration), two heads for the selection mask
+    and 2048 sampled query rows on each of two heads for the attention."""
     wl = svg2_synth.WORKLOADS[name]
     q, k, v = svg2_synth.generate(wl)
     Q, K, V = to_dev(q), to_dev(k), to_dev(v)
     del q, k, v
-    d = wl.d
-    _, _, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, wl.top_p)
-    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, wl.top_p, ex["q_centroids"], ex["k_centroids"],
+    d, N = wl.d, wl.N
+    _, _, ex0 = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, wl.top_p)
+    cache_q, cache_k = ex0["q_centroids"].clone(), ex0["k_centroids"].clone()
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, wl.top_p, ex0["q_centroids"], ex0["k_centroids"],
                                          warm=True, debug=True)
     torch.cuda.synchronize()
-    dens = pairs.double() / (wl.N * wl.N)
+    dens = pairs.double() / (N * N)
     assert 0.02 < float(dens.mean()) < 0.9
+    # ---- P2/P3: the warm call's two Lloyd iterations, teacher-forced (one head, both roles)
+    h = wl.H // 2
+    for X, C, cache, key in ((Q, wl.Cq, cache_q, "q"), (K, wl.Ck, cache_k, "k")):
+        Xh = X[:, h:h + 1].contiguous()
+        X64 = to_f64(Xh)[0, 0]
+        cent = cache[:, h:h + 1].contiguous()
+        for it in range(2):
+            c_in = cent.clone()
+            labels, sizes, cent = svg2.kmeans(Xh, C, 1, centroids=cent)
+            c64 = c_in.cpu().numpy().astype(np.float64)[0, 0]
+            gl = labels.cpu().numpy()[0, 0]
+            nbad, nontie = label_mismatches_are_ties(X64, c64, gl)
+            assert nontie == 0, f"{name} role {key} iteration {it}: {nontie} label mismatches outside the tie band"
+            assert nbad <= N // 10000, f"{name} role {key} iteration {it}: {nbad} near-tie flips"
+            # the update from the GPU's labels: exact means, f32-rounded, bit-exact (R4, R22)
+            oc = np.zeros((C, d))
+            np.add.at(oc, gl, X64)
+            osz = np.bincount(gl, minlength=C)
+            assert np.array_equal(sizes.cpu().numpy()[0, 0], osz)
+            ref = np.where(osz[:, None] > 0, oc / np.maximum(osz, 1)[:, None], c64).astype(np.float32)
+            if nbad == 0:
+                ol, ocen, osz2 = oracle_mod.kmeans(X64, C, 1, init=c64)
+                assert np.array_equal(ol, gl) and np.array_equal(osz2, osz)
+                ref = ocen.astype(np.float32)
+            assert np.array_equal(cent.cpu().numpy()[0, 0], ref), f"{name} role {key} iteration {it}: update"
+        # the fused call ran the same two iterations on this head: same labels and cache bits
+        assert np.array_equal(ex[f"{key}_labels"].cpu().numpy()[0, h], gl)
+        assert torch.equal(ex[f"{key}_centroids"][0, h], cent[0, 0])
+    # ---- P1/P4/P5 on two heads
     for h in (0, wl.H - 1):
-        rows = svg2_synth.sample_rows(wl.N, 256, seed=h)
-        Q64, K64, V64 = (to_f64(t[0, h]) for t in (Q, K, V))
         lq, lk, m = (ex[n].cpu().numpy()[0, h] for n in ("q_labels", "k_labels", "mask"))
+        sq, sk = np.bincount(lq, minlength=wl.Cq), np.bincount(lk, minlength=wl.Ck)
+        # permutations and offsets of the final labels, bit-exact
+        for lab, C, key in ((lq, wl.Cq, "q"), (lk, wl.Ck, "k")):
+            p_ref, o_ref = oracle_mod.permute(lab, C)
+            assert np.array_equal(ex[f"{key}_perm"].cpu().numpy()[0, h], p_ref)
+            assert np.array_equal(ex[f"{key}_offsets"].cpu().numpy()[0, h], o_ref)
+        # selection on the GPU's f32 centroids and sizes (R22): mask bit-exact except R17 near-ties
+        om, opairs, S, W, Z = oracle_mod.select_topp(ex["q_centroids"].cpu().numpy()[0, h].astype(np.float64),
+                                                     ex["k_centroids"].cpu().numpy()[0, h].astype(np.float64),
+                                                     sq, sk, d, f32scale(d), wl.top_p, return_tables=True)
+        nrows, nontie = mask_mismatch_rows_are_ties(W, Z, sk, wl.top_p, m, om)
+        assert nontie == 0, f"{name} head {h}: {nontie} mask rows differ off a near-tie"
+        if nrows == 0:
+            assert int(pairs[0, h]) == opairs
+        assert int(pairs[0, h]) == int((sq[:, None] * sk[None, :] * m).sum())
+        # attention on 2048 sampled rows, fed the GPU's labels and mask
+        rows = svg2_synth.sample_rows(N, 2048, seed=h)
+        Q64, K64, V64 = (to_f64(t[0, h]) for t in (Q, K, V))
         ref = oracle_mod.attention_rows(Q64, K64, V64, f32scale(d), rows=rows, lq=lq, lk=lk, mask=m)
         check_attention(O[0, h][torch.from_numpy(rows).cuda()], ref, f"{name} head {h}")
-        # permutation and offsets of the final labels, bit-exact
-        p_ref, o_ref = oracle_mod.permute(lk, wl.Ck)
-        assert np.array_equal(ex["k_perm"].cpu().numpy()[0, h], p_ref)
-        assert np.array_equal(ex["k_offsets"].cpu().numpy()[0, h], o_ref)
-        # the returned centroids are the exact means of the returned clusters (f32-rounded)
-        ol, oc, osz = oracle_mod.kmeans(Q64, wl.Cq, 1, init=ex["q_centroids"].cpu().numpy()[0, h].astype(np.float64))
-        assert np.array_equal(np.bincount(lq, minlength=wl.Cq), ex["q_offsets"].cpu().numpy()[0, h][1:] -
-                              ex["q_offsets"].cpu().numpy()[0, h][:-1])
 
 
 @pytest.mark.parametrize("init", ["strided", "kmeans++"])
