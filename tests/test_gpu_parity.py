@@ -78,32 +78,41 @@ def test_kmeans_teacher_forced(svg2, oracle_mod, N, d, C):
 
 @pytest.mark.parametrize("N,d,C,iters", [(1024, 64, 16, 5), (5000, 128, 100, 3)])
 def test_kmeans_objective(svg2, oracle_mod, N, d, C, iters):
-    """The Lloyd objective the library reports per iteration: equal to the oracle's J_assign / J_post
-    (same labels: the cold strided run of both sides) within 1e-9 relative, and J_assign(t) >= J_post(t) >=
-    J_assign(t+1) on the GPU side within 1e-12 relative.  Also through the fused call's debug."""
+    """The Lloyd objective the library reports per iteration, teacher-forced (P3): each iteration is
+    re-run by the oracle from the GPU's f32 input centroids, and (J_assign, J_post) agree within 1e-9 relative (R16
+    near-tie flips: 1e-7).  The multi-iteration call reports the same values bit for bit, and on the GPU side
+    J_assign(t) >= J_post(t) >= J_assign(t+1) within 1e-12 relative.  Also through the fused call's debug."""
     q, k, _ = random_qkv(2, 2, N, N, d, seed=N + 3, groups=16)
     X = to_dev(q)
     labels, sizes, cent, obj = svg2.kmeans(X, C, iters, return_objective=True)
-    obj = obj.cpu().numpy()
     assert obj.shape == (iters, 2, 2, 2)
-    for b in range(2):
-        for h in range(2):
-            ol, oc, osz, ja, jp = oracle_mod.kmeans(to_f64(X)[b, h], C, iters, return_objective=True)
-            # an R16 near-tie flip in an earlier iteration moves J by ~1e-5 of one row's distance: looser bound then
-            rtol = 1e-9 if np.array_equal(labels.cpu().numpy()[b, h], ol) else 1e-6
-            ga, gp = obj[:, b, h, 0], obj[:, b, h, 1]
-            np.testing.assert_allclose(ga, ja, rtol=rtol)
-            np.testing.assert_allclose(gp, jp, rtol=rtol)
-            for t in range(iters):
-                assert gp[t] <= ga[t] * (1 + 1e-12)
-                if t + 1 < iters:
-                    assert ga[t + 1] <= gp[t] * (1 + 1e-12)
+    X64 = to_f64(X)
+    c = torch.from_numpy(X64[:, :, (np.arange(C) * N) // C].astype(np.float32)).cuda().contiguous()
+    for t in range(iters):
+        c_in = c.clone()
+        lab_t, _, c, obj_t = svg2.kmeans(X, C, 1, centroids=c, return_objective=True)
+        assert torch.equal(obj_t[0], obj[t]), f"iteration {t}: the multi-iteration call differs"
+        for b in range(2):
+            for h in range(2):
+                c64 = c_in.cpu().numpy().astype(np.float64)[b, h]
+                ol, _, _, ja, jp = oracle_mod.kmeans(X64[b, h], C, 1, init=c64, return_objective=True)
+                nbad, nontie = label_mismatches_are_ties(X64[b, h], c64, lab_t.cpu().numpy()[b, h])
+                assert nontie == 0
+                rtol = 1e-9 if nbad == 0 else 1e-7
+                g = obj_t.cpu().numpy()[0, b, h]
+                np.testing.assert_allclose(g, [ja[0], jp[0]], rtol=rtol)
+    o = obj.cpu().numpy()
+    for t in range(iters):
+        assert np.all(o[t, ..., 1] <= o[t, ..., 0] * (1 + 1e-12))
+        if t + 1 < iters:
+            assert np.all(o[t + 1, ..., 0] <= o[t, ..., 1] * (1 + 1e-12))
     Q, K = to_dev(q), to_dev(k)
     _, _, ex = svg2.sparse_attention(Q, K, K, C, C, iters, 0.9, debug=True)
     torch.cuda.synchronize()
-    assert torch.equal(ex["q_objective"].cpu(), torch.from_numpy(obj))
+    # the fused call's last update is the gather pass (32-row chunks, not 64): same J up to fp64 rounding order
+    torch.testing.assert_close(ex["q_objective"], obj, rtol=1e-12, atol=0)
     _, _, _, kobj = svg2.kmeans(K, C, iters, return_objective=True)
-    assert torch.equal(ex["k_objective"], kobj)
+    torch.testing.assert_close(ex["k_objective"], kobj, rtol=1e-12, atol=0)
 
 
 def test_kmeans_update_deterministic_wide_exponent_spread(svg2):
