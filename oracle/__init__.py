@@ -10,6 +10,7 @@ function citing the PAPER.md passage it follows.  This module only marshals nump
 
 Per-(b,h) functions:
     kmeans(X, C, iters, init=None)            PAPER.md:259, 322-326   (Lloyd, strided cold init R2)
+    identification.*                          recall / density / miss / waste / PSNR / position blocks (8(f) row 3)
     assign(X, centroids)                      one assign step + best/second distances (R16 tie bands)
     permute(labels, C)                        PAPER.md:275            (stable counting sort)
     select_topp(cq, ck, sq, sk, d, scale, p)  PAPER.md:296-315        (Eq. 1, Eq. 2, top-p)

@@ -96,11 +96,18 @@ def test_kmeans_objective(svg2, oracle_mod, N, d, C, iters):
             for h in range(2):
                 c64 = c_in.cpu().numpy().astype(np.float64)[b, h]
                 ol, _, _, ja, jp = oracle_mod.kmeans(X64[b, h], C, 1, init=c64, return_objective=True)
-                nbad, nontie = label_mismatches_are_ties(X64[b, h], c64, lab_t.cpu().numpy()[b, h])
+                gl = lab_t.cpu().numpy()[b, h]
+                nbad, nontie = label_mismatches_are_ties(X64[b, h], c64, gl)
                 assert nontie == 0
-                rtol = 1e-9 if nbad == 0 else 1e-7
                 g = obj_t.cpu().numpy()[0, b, h]
-                np.testing.assert_allclose(g, [ja[0], jp[0]], rtol=rtol)
+                if nbad == 0:
+                    np.testing.assert_allclose(g, [ja[0], jp[0]], rtol=1e-9)
+                else:  # R16 flips: J_assign moves by at most the tie gaps; J_post is that of the GPU's own clusters
+                    slack = nbad * 1e-5 * float(((X64[b, h] ** 2).sum(1)).max() + (c64 ** 2).sum(1).max())
+                    assert abs(g[0] - ja[0]) <= slack + 1e-9 * ja[0]
+                    c_new = c.cpu().numpy().astype(np.float64)[b, h]
+                    jpost = float(((X64[b, h] - c_new[gl]) ** 2).sum())
+                    np.testing.assert_allclose(g[1], jpost, rtol=1e-9)
     o = obj.cpu().numpy()
     for t in range(iters):
         assert np.all(o[t, ..., 1] <= o[t, ..., 0] * (1 + 1e-12))

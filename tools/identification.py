@@ -9,7 +9,8 @@ On sampled query rows of a few heads, against the exact dense attention distribu
   * position-block baselines: 128-query x 64-key blocks of consecutive tokens, block scores from
     mean-pooled Q and mean- or max-pooled K, the same top-p rule; also cut AFTER the semantic permutation.
 Metrics per method at each p: density, recall (selected P mass, averaged over rows), critical-token miss rate and
-waste against the oracle set at the same p.  Writes profiles/identification_r01.json.  Uses no oracle/ code.
+waste against the oracle set at the same p.  Writes profiles/identification_r02.json.  Uses no oracle/ code; tests/test_identification.py reproduces its metric
+and position-block functions with oracle/identification.py on the tiny config.
 """
 import argparse
 import json
@@ -99,7 +100,7 @@ def main():
     ap.add_argument("--workload", default="wan480p")
     ap.add_argument("--heads", type=int, default=4)
     ap.add_argument("--rows", type=int, default=1024)
-    ap.add_argument("--out", default="profiles/identification_r01.json")
+    ap.add_argument("--out", default="profiles/identification_r02.json")
     args = ap.parse_args()
     wl = svg2_synth.WORKLOADS[args.workload]
     heads = list(range(args.heads))
