@@ -2,6 +2,7 @@
 // touched on error), workspace carving, and the enqueue of the kernels of svg2_*.cu on the caller's stream.
 #include <cuda_runtime.h>
 #include <cmath>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: stage ranges for nsys / ncu --nvtx (no-ops without a tool)
 #include "../../include/svg2.h"
 #include "internal.h"
 
@@ -112,8 +113,13 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
     if (dbg->k_offsets) w.off_k = dbg->k_offsets;
     if (dbg->mask) w.mask = dbg->mask;
   }
+  // stage boundaries: the caller's timing events (dbg) and NVTX ranges around each stage's enqueue
+  static const char* const kStageNames[7] = {"svg2 kmeans K (forked stream)", "svg2 kmeans Q", "svg2 permute V (fp8)",
+                                             "svg2 select_topp", "svg2 worklist", "svg2 varblock_attention", ""};
   auto mark = [&](int k) {
     if (dbg && dbg->events[k]) cudaEventRecord(static_cast<cudaEvent_t>(dbg->events[k]), s);
+    if (k > 0 && k < 7) nvtxRangePop();
+    if (k < 6) nvtxRangePushA(kStageNames[k]);
   };
   const int BH = dm.B * dm.H;
   const bool warm = cfg->flags & SVG2_WARM_START;

@@ -55,6 +55,9 @@ WORKLOADS = {
     "tiny": Workload("tiny", 0, 1, 1, (4, 16, 16), 64, 16, 32, 0.9, 5, 16, 6.0),
     "hunyuan720p": Workload("hunyuan720p", 1, 1, 24, (33, 45, 80), 128, 100, 500, 0.9, 5, 64, 8.0),
     "wan720p": Workload("wan720p", 2, 1, 40, (21, 45, 80), 128, 100, 500, 0.9, 5, 64, 8.0),
+    # HunyuanVideo calibrated to the paper's density (25.45%): a = 8.1 gives 0.258 on the
+    # first warm call and ~0.25 in steady state (profiles/r02_calibration_hunyuan720p.jsonl); same seeds as above
+    "hunyuan720p_r25": Workload("hunyuan720p_r25", 1, 1, 24, (33, 45, 80), 128, 100, 500, 0.9, 5, 64, 8.1),
     "wan480p": Workload("wan480p", 4, 1, 40, (21, 30, 52), 128, 100, 500, 0.9, 5, 64, 8.0),
 }
 
