@@ -67,8 +67,10 @@ typedef struct {
                                  picks reproducible bit for bit.  Ignored with SVG2_WARM_START.  Costs C passes over
                                  X (the expense the centroid cache avoids). */
 #define SVG2_FP8_PV 4u /* the "+FP8" variant as DESIGN.md R26 reads it: P and V enter the PV
-                          product as e4m3 (V with a per-(b,h) scale 448 / max|V|, P unscaled), fp32 accumulation;
-                          QK^T, the softmax and the output stay bf16 / fp32.  d = 128 only. */
+                          product as e4m3 -- V with per-(b,h, channel) scales 448 / max_n |V_nc| undone in the epilogue,
+                          P with a per-row power-of-two scale (2^6 over the running max, lazy rescale at +2) that
+                          cancels in O / l -- fp32 accumulation; QK^T, the softmax and the output stay bf16 / fp32.
+                          d = 128 only. */
 
 typedef struct {
   int32_t Cq, Ck;  /* query / key cluster counts (paper default 100 / 500) */

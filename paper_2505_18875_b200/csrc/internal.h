@@ -122,7 +122,8 @@ cudaError_t launch_stable_sort(const int32_t* labels, int BH, int N, int C, Sort
 cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const void* X0, void* X0p,
                                const void* X1, void* X1p, cudaStream_t s);
 cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int N, int d, void* O, cudaStream_t s);
-// FP8 PV: per-head |x| max (amax, f32 bits) and the gather of X[perm] rounded to e4m3 with scale 448 / amax
+// FP8 PV: per-(head, channel) |x| max (amax [BH, d], f32 bits) and the gather of X[perm] rounded to e4m3 with channel
+// scales 448 / amax_c
 cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, const void* X, void* Xq, uint32_t* amax,
                                     cudaStream_t s);
 // k-means cold-start options (DESIGN R2, R25): strided rows, or k-means++ with the R25 generator

@@ -54,7 +54,7 @@ struct FusedWs {
   int32_t *lab_q, *lab_k, *perm_q, *perm_k, *off_q, *off_k, *size_q, *size_k;
   void *Qp, *Kp, *Vp;
   uint8_t* mask;
-  uint32_t* v_amax;  // FP8 PV: per-head max |V| (f32 bits)
+  uint32_t* v_amax;  // FP8 PV: per-(head, channel) max |V| (f32 bits) [BH, d]
   KmeansWs km_q, km_k;  // per-role k-means scratch: the two roles may run concurrently
   AttnWs attn;
 };
@@ -74,7 +74,7 @@ FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) 
   w.Kp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.Vp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.mask = c.take<uint8_t>(BH * cfg.Cq * cfg.Ck);
-  w.v_amax = c.take<uint32_t>(BH);
+  w.v_amax = c.take<uint32_t>(BH * dm.d);
   w.km_q = carve_kmeans(c, int(BH), dm.Nq, cfg.Cq);
   w.km_k = carve_kmeans(c, int(BH), dm.Nk, cfg.Ck);
   w.attn = carve_attn(c, int(BH), dm.Nq, dm.Nk, cfg.Cq, cfg.Ck);

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           mbar_wait(&bars.item_full[islot], iph);
-          it = item_slot[islot];
+          it = read_slot_bcast(&item_slot[islot]);
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
         }
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (void)tr_first;
       while (true) {
         mbar_wait_warp(&bars.item_full[islot], iph);
-        const int4 it = item_slot[islot];
+        const int4 it = read_slot_bcast(&item_slot[islot]);
         __syncwarp();
         mbar_arrive_warp(&bars.item_empty[islot]);
         if (++islot == 2) {
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     while (true) {
       mbar_wait(&bars.item_full[islot], iph);
-      const int4 it = item_slot[islot];
+      const int4 it = read_slot_bcast(&item_slot[islot]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
       if (++islot == 2) {
@@ -557,9 +557,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (g == 1) merge_ml[rloc] = make_float2(m_used, l);
         tc_fence_before();
         named_bar_sync(kBarMerge, 256);
+        float2 mlb = make_float2(0.f, 0.f);
+        if (g == 0) mlb = merge_ml[rloc];
+        // warpgroup b may write merge_ml again only after a has read it (the o_full / o_empty chain already orders
+        // this; the second barrier makes it explicit at the cost of one 256-thread sync per split item)
+        named_bar_sync(kBarMerge, 256);
         if (g == 1) continue;
         tc_fence_after();
-        const float2 mlb = merge_ml[rloc];
         const float m = fmaxf(m_used, mlb.x);
         const float wa = ex2_approx(m_used - m), wb = ex2_approx(mlb.x - m);
         const float lt = l * wa + mlb.y * wb;

@@ -37,6 +37,13 @@ constexpr int kBoxKinds = 5;                // box heights 8, 16, 32, 64, 128 ro
 // more than this, so P <= 2^threshold between rescales.  P is bf16 (relative precision at any magnitude) and O / l
 // accumulate in fp32, so 2^20 leaves > 10^20 headroom for 10^5 keys.
 constexpr float kRescaleThreshold = 8.0f;
+// FP8 PV: the per-row P scale.  P enters e4m3 as p' = 2^(s*scale*log2e - m_used + kPShift), with the lazy rescale
+// threshold lowered to kRescaleThresholdFp8 so that p' <= 2^(threshold + shift) = 256 <= 448 (e4m3 max): weights
+// down to 2^-(6+shift) = 2^-12 of the running max stay normal e4m3 (3-bit mantissa) instead of 2^-6, and only weights
+// below 2^-16 of it flush to zero (unscaled P lost everything under 2^-10).  l sums the same scaled p', so
+// the shift cancels in O / l; lse subtracts it.
+constexpr float kRescaleThresholdFp8 = 2.0f, kPShift = 6.0f;
+static_assert(kRescaleThresholdFp8 + kPShift <= 8.0f, "scaled P must stay <= 256 < 448 (e4m3 max)");
 constexpr uint64_t kFullTileWord = 0x8888888888888888ull;
 // setmaxnreg budget: the launch reserves 168 regs x 384 threads; the control warpgroup (warps 8-11) shrinks to 72
 // and the two softmax warpgroups grow to 216.  The sum must not exceed the reservation or .inc never returns.
@@ -83,7 +90,7 @@ struct Params {
   float* lse;
   int Nq;
   float scale_log2;
-  const uint32_t* v_amax;  // kFp8: per-head max |V| (f32 bits); O is scaled by amax / 448 in the epilogue
+  const uint32_t* v_amax;  // kFp8: per-(head, channel) max |V| [BH, D] (f32 bits); O channel c is scaled by amax_c / 448
 };
 
 // Loads one 16-group tile of the item's key stream into a K or V stage.  Lanes 0..ngt-1 hold one group each; a
@@ -238,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dv0 = desc_mnmajor_sw128(smem_u32(sV), C::kBlockBytes);
       while (true) {
         mbar_wait_warp(&bars.item_full[islot], iph);
-        const int4 it = item_slot[islot];
+        const int4 it = read_slot_bcast(&item_slot[islot]);
         __syncwarp();
         mbar_arrive_warp(&bars.item_empty[islot]);
         if (++islot == 2) {
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t sph = 0, oph = 0, islot = 0, iph = 0;
     while (true) {
       mbar_wait(&bars.item_full[islot], iph, 18);
-      const int4 it = item_slot[islot];
+      const int4 it = read_slot_bcast(&item_slot[islot]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
       if (++islot == 2) {
@@ -453,7 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mt = fmaxf(mx0, mx1) * sl2;
         if (t == t_first) {
           m_used = mt;
-        } else if (__any_sync(0xffffffffu, rloc < nrows && mt > m_used + kRescaleThreshold)) {
+        } else if (__any_sync(0xffffffffu,
+                              rloc < nrows && mt > m_used + (kFp8 ? kRescaleThresholdFp8 : kRescaleThreshold))) {
           // only rows of the cluster vote: the tile's padding rows hold whatever follows the cluster in Q'
           // (another cluster or head), and must not change how the cluster's rows are rounded
           // warp-uniform branch (tcgen05.ld/st are .sync.aligned); rows whose max did not grow get alpha = 1
@@ -472,7 +480,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = m_new;
         }
         // p = 2^(s * scale*log2e - m): FFMA2 on pairs, MUFU ex2 per element, FADD2 row sums, bf16x2 packs
-        const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(-m_used, -m_used);
+        const float pshift = kFp8 ? kPShift : 0.f;
+        const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(pshift - m_used, pshift - m_used);
         uint64_t lsum2 = f2(0.f, 0.f);
         auto exp_store = [&](const uint32_t(&a)[32], int c) {
           uint32_t pk[16];
@@ -524,15 +533,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Warpgroup a releases both O accumulators (o_empty counts 4 arrivals, one per warp of a).
         if (g == 1) merge_ml[rloc] = make_float2(m_used, l);
         named_bar_sync(1, 256);
+        float2 mlb = make_float2(0.f, 0.f);
+        if (g == 0) mlb = merge_ml[rloc];
+        named_bar_sync(1, 256);  // b writes merge_ml again only after a has read it
         if (g == 1) {
           continue;
         }
-        const float2 mlb = merge_ml[rloc];
         const float m = fmaxf(m_used, mlb.x);
         const float wa = ex2_approx(m_used - m), wb = ex2_approx(mlb.x - m);
         const float lt = l * wa + mlb.y * wb;
-        const float vsc = kFp8 ? __uint_as_float(__ldg(p.v_amax + (it.w & kItemBhMask))) * (1.f / 448.f) : 1.f;
-        const float ca = wa / lt * vsc, cb = wb / lt * vsc;
+        const float ca = wa / lt, cb = wb / lt;
+        const uint32_t* vam = kFp8 ? p.v_amax + size_t(it.w & kItemBhMask) * D : nullptr;
         const long long row_flat = (long long)it.x + rloc;
         long long dst = row_flat;
         if (rloc < nrows && p.q_perm) dst = (long long)(it.w & kItemBhMask) * p.Nq + __ldg(p.q_perm + row_flat);
@@ -549,14 +560,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int v = 0; v < 4; ++v) {
               float r[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
+              for (int e = 0; e < 8; ++e) {
                 r[e] = __uint_as_float(oa[8 * v + e]) * ca + __uint_as_float(ob[8 * v + e]) * cb;
+                if (kFp8) r[e] *= __uint_as_float(__ldg(vam + 32 * c + 8 * v + e)) * (1.f / 448.f);
+              }
               orow[4 * c + v] = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
                                            pack_bf16x2(r[6], r[7]));
             }
           }
         }
-        if (rloc < nrows && p.lse) p.lse[dst] = (m + __log2f(lt)) * 0.69314718055994531f;
+        if (rloc < nrows && p.lse) p.lse[dst] = (m - (kFp8 ? kPShift : 0.f) + __log2f(lt)) * 0.69314718055994531f;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -565,7 +578,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      const float inv_l = (kFp8 ? __uint_as_float(__ldg(p.v_amax + (it.w & kItemBhMask))) * (1.f / 448.f) : 1.f) / l;
+      const float inv_l = 1.f / l;
+      const uint32_t* vam = kFp8 ? p.v_amax + size_t(it.w & kItemBhMask) * D : nullptr;
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
       if (rloc < nrows && p.q_perm) {
@@ -578,6 +592,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t o[32];
         tmem_ld32(tO + 32 * c, o);
         tmem_wait_ld();
+        if (kFp8) {  // per-channel V scale: o_c *= amax_c / 448
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            o[e] = __float_as_uint(__uint_as_float(o[e]) * (__uint_as_float(__ldg(vam + 32 * c + e)) * (1.f / 448.f)));
+        }
         if (rloc < nrows) {
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
@@ -590,7 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (rloc < nrows && p.lse) p.lse[dst] = (m_used + __log2f(l)) * 0.69314718055994531f;
+      if (rloc < nrows && p.lse)
+        p.lse[dst] = (m_used - (kFp8 ? kPShift : 0.f) + __log2f(l)) * 0.69314718055994531f;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_empty[g]);

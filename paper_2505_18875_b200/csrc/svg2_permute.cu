@@ -169,26 +169,39 @@ __global__ void k_scatter_rows(const uint4* __restrict__ Op, const int32_t* __re
   }
 }
 
-// FP8 PV path: per (b,h) the largest |x| (bf16 -> f32, as float bits: non-negative floats order like uints)
-__global__ void k_absmax(const uint4* __restrict__ X, long long vec_per_bh, uint32_t* __restrict__ amax) {
+// FP8 PV path: per (b,h) and channel c the largest |x_c| (bf16 -> f32, as float bits: non-negative floats order like
+// uints).  The grid stride is a multiple of the vectors per row, so a thread always reads the same 8 channels.
+__global__ void k_absmax(const uint4* __restrict__ X, long long vec_per_bh, int vec_per_row,
+                         uint32_t* __restrict__ amax) {
   const int bh = blockIdx.y;
   const uint4* Xb = X + size_t(bh) * vec_per_bh;
-  float m = 0.f;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < vec_per_bh;
-       t += (long long)gridDim.x * blockDim.x) {
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  float m[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) m[e] = 0.f;
+  for (long long t = t0; t < vec_per_bh; t += (long long)gridDim.x * blockDim.x) {
     const uint4 u = __ldg(Xb + t);
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 f = __bfloat1622float2(h[e]);
-      m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+      m[2 * e] = fmaxf(m[2 * e], fabsf(f.x));
+      m[2 * e + 1] = fmaxf(m[2 * e + 1], fabsf(f.y));
     }
   }
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax + bh, __float_as_uint(m));
+  // lanes l and l ^ o (o >= vec_per_row) hold the same channels
+  for (int o = 16; o >= vec_per_row; o >>= 1)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m[e] = fmaxf(m[e], __shfl_xor_sync(0xffffffffu, m[e], o));
+  if ((threadIdx.x & 31) < vec_per_row) {
+    const int c0 = int(t0 % vec_per_row) * 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) atomicMax(amax + size_t(bh) * vec_per_row * 8 + c0 + e, __float_as_uint(m[e]));
+  }
 }
 
-// FP8 PV path: V' = V[perm] rounded to e4m3 with the head's scale 448 / amax (448 = largest finite e4m3)
+// FP8 PV path: V' = V[perm] rounded to e4m3, channel c scaled by 448 / amax_c of its head (448 = largest finite e4m3);
+// the attention epilogue multiplies output channel c by amax_c / 448
 __global__ void k_gather_rows_e4m3(const int32_t* __restrict__ perm, long long rows, int N, int vec_per_row,
                                    const uint4* __restrict__ X, uint2* __restrict__ Xq,
                                    const uint32_t* __restrict__ amax) {
@@ -198,15 +211,15 @@ __global__ void k_gather_rows_e4m3(const int32_t* __restrict__ perm, long long r
     const long long r = t / vec_per_row;
     const int v = int(t - r * vec_per_row);
     const long long bh = r / N;
-    const float a = __uint_as_float(__ldg(amax + bh));
-    const float sc = a > 0.f ? 448.f / a : 1.f;
     const uint4 u = __ldg(X + (bh * N + __ldg(perm + r)) * vec_per_row + v);
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const uint32_t* am = amax + (bh * vec_per_row + v) * 8;
     uint32_t q[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+      const float a0 = __uint_as_float(__ldg(am + 2 * e)), a1 = __uint_as_float(__ldg(am + 2 * e + 1));
       const float2 f = __bfloat1622float2(h[e]);
-      q[e] = pack_e4m3x2(f.x * sc, f.y * sc);
+      q[e] = pack_e4m3x2(f.x * (a0 > 0.f ? 448.f / a0 : 1.f), f.y * (a1 > 0.f ? 448.f / a1 : 1.f));
     }
     Xq[r * vec_per_row + v] = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
   }
@@ -247,12 +260,12 @@ cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, c
                                     cudaStream_t s) {
   const long long rows = (long long)BH * N;
   const int vpr = d / 8;
-  cudaMemsetAsync(amax, 0, size_t(BH) * sizeof(uint32_t), s);
+  cudaMemsetAsync(amax, 0, size_t(BH) * d * sizeof(uint32_t), s);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int per_bh = (sms * 8 + BH - 1) / BH;
-  k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(static_cast<const uint4*>(X), (long long)N * vpr, amax);
+  k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(static_cast<const uint4*>(X), (long long)N * vpr, vpr, amax);
   k_gather_rows_e4m3<<<copy_grid(rows * vpr), 256, 0, s>>>(perm, rows, N, vpr, static_cast<const uint4*>(X),
                                                            static_cast<uint2*>(Xq), amax);
   return cudaGetLastError();

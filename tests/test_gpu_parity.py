@@ -657,3 +657,27 @@ def test_fp8_pv_within_e4m3_bound(svg2, oracle_mod, case):
         errs.append(err)
         mags.append(mag)
     assert np.concatenate(errs).mean() <= FP8_MEAN_REL * np.concatenate(mags).mean()
+
+
+def test_fp8_pv_diffuse_rows_unbiased(svg2, oracle_mod):
+    """FP8 PV on diffuse attention: scores spread over ~10 nats and long key streams (few clusters, top-p
+    0.99), V with a large common offset, so keys far below the running max carry a visible share of the mass.  The
+    per-row P scale (2^6, lazy rescale at +2) keeps weights down to 2^-12 of the max normal in e4m3; the output stays
+    within the e4m3 first-order bound and is unbiased: the signed error averages to < 2^-8 of the mean |o| (unscaled
+    P flushed every weight under 2^-10 of the running max to 0 while l still counted it, shrinking O toward 0)."""
+    rng = np.random.default_rng(81)
+    N, d = 8000, 128
+    q = svg2_synth.f32_to_bf16_bits((1.58 * rng.standard_normal((1, 1, N, d))).astype(np.float32))
+    k = svg2_synth.f32_to_bf16_bits((1.58 * rng.standard_normal((1, 1, N, d))).astype(np.float32))
+    v = svg2_synth.f32_to_bf16_bits((3.0 + rng.standard_normal((1, 1, N, d))).astype(np.float32))
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O8, pairs, ex = svg2.sparse_attention(Q, K, V, 4, 8, 2, 0.99, debug=True, fp8=True)
+    rows = np.arange(0, N, 7)
+    lq, lk, m = (ex[key][0, 0].cpu().numpy() for key in ("q_labels", "k_labels", "mask"))
+    Q64, K64, V64 = to_f64(Q)[0, 0], to_f64(K)[0, 0], to_f64(V)[0, 0]
+    assert float(pairs[0, 0]) / (N * N) > 0.5  # long key streams
+    ref = oracle_mod.attention_rows(Q64, K64, V64, f32scale(d), rows=rows, lq=lq, lk=lk, mask=m)
+    mag = oracle_mod.attention_rows(Q64, K64, np.abs(V64), f32scale(d), rows=rows, lq=lq, lk=lk, mask=m)
+    err = to_f64(O8)[0, 0][rows] - ref
+    assert np.all(np.abs(err) <= FP8_REL * mag + FP8_ABS), f"worst excess {np.max(np.abs(err) - FP8_REL * mag):.3e}"
+    assert abs(err.mean()) <= 2.0 ** -8 * np.abs(ref).mean(), f"bias {err.mean():.3e} vs mean |o| {np.abs(ref).mean():.3e}"

@@ -60,11 +60,15 @@ def run_point(Q, K, V, ref, wl, Cq, Ck, p, reps=3):
     svg2.sparse_attention(Q, K, V, Cq, Ck, 2, p, cq, ck, warm=True)
     torch.cuda.synchronize()
     t_call = t_attn = 0.0
+    names = ["kmeans_k_fork", "kmeans_q_join", "permute_fp8", "select_topp", "worklist", "attention", "end"]
+    stages = {n: 0.0 for n in names}
     for _ in range(reps):
         O, pairs, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, 2, p, cq, ck, warm=True, events=ev, debug=True)
         torch.cuda.synchronize()
         t_call += ev[0].elapsed_time(ev[7]) / reps
         t_attn += ev[5].elapsed_time(ev[6]) / reps
+        for i, n in enumerate(names):
+            stages[n] += ev[i].elapsed_time(ev[i + 1]) / reps
     B, H, N, d = Q.shape
     dens = float(pairs.double().sum()) / (B * H * N * N)
     alg, exe, static = tile_work(ex["q_offsets"], ex["k_offsets"], ex["mask"])
@@ -72,14 +76,15 @@ def run_point(Q, K, V, ref, wl, Cq, Ck, p, reps=3):
             "eff_tflops": 4.0 * N * N * d * B * H / (t_call * 1e-3) / 1e12,
             "attn_executed_tflops": 4.0 * d * float(pairs.double().sum()) / (t_attn * 1e-3) / 1e12,
             "tile_work_multiplier": exe / alg, "static128_multiplier": static / alg,
-            "static_over_packed": static / exe, **accuracy(O, ref)}
+            "static_over_packed": static / exe, "stages_ms": stages, **accuracy(O, ref)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="wan480p")
     ap.add_argument("--heads", type=int, default=40)
-    ap.add_argument("--out", default="profiles/sweep_r01.json")
+    ap.add_argument("--out", default="profiles/sweep_r02.json")
+    ap.add_argument("--points", default=None, help="only these Cq:Ck pairs at p = 0.9, e.g. 200:4000,400:500")
     args = ap.parse_args()
     wl = svg2_synth.WORKLOADS[args.workload]
     q, k, v = svg2_synth.generate(wl, heads=range(args.heads))
@@ -97,6 +102,13 @@ def main():
         t_dense = s.elapsed_time(e)
     res = {"workload": wl.name, "heads": args.heads, "N": wl.N, "dense_ms_sdpa": t_dense, "topp_sweep": [],
            "cluster_sweep": []}
+    if args.points:
+        for pt in args.points.split(","):
+            Cq, Ck = (int(x) for x in pt.split(":"))
+            r = run_point(Q, K, V, ref, wl, Cq, Ck, 0.9)
+            r["speedup_vs_dense"] = t_dense / r["ms_call"]
+            print(json.dumps(r), flush=True)
+        return
     for p in [0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 1.0]:
         r = run_point(Q, K, V, ref, wl, 100, 500, p)
         r["speedup_vs_dense"] = t_dense / r["ms_call"]
