@@ -93,18 +93,6 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// A work-item slot written by another warp and published through an mbarrier: read by lane 0 only and broadcast, so the
-// read is program-ordered before the lane-0 (or elect.sync lane-0) arrive that frees the slot for the next write.
-__device__ __forceinline__ int4 read_slot_bcast(const int4* slot) {
-  int4 v = make_int4(0, 0, 0, 0);
-  if ((threadIdx.x & 31) == 0) v = *slot;
-  v.x = __shfl_sync(0xffffffffu, v.x, 0);
-  v.y = __shfl_sync(0xffffffffu, v.y, 0);
-  v.z = __shfl_sync(0xffffffffu, v.z, 0);
-  v.w = __shfl_sync(0xffffffffu, v.w, 0);
-  return v;
-}
-
 // one arrive per warp, issued by an elected lane (warp-convergent code)
 __device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
   asm volatile(

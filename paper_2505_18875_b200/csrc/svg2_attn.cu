@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           mbar_wait(&bars.item_full[islot], iph);
-          it = read_slot_bcast(&item_slot[islot]);
+          it = item_slot[islot];
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
         }
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       (void)tr_first;
       while (true) {
         mbar_wait_warp(&bars.item_full[islot], iph);
-        const int4 it = read_slot_bcast(&item_slot[islot]);
+        const int4 it = item_slot[islot];
         __syncwarp();
         mbar_arrive_warp(&bars.item_empty[islot]);
         if (++islot == 2) {
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     while (true) {
       mbar_wait(&bars.item_full[islot], iph);
-      const int4 it = read_slot_bcast(&item_slot[islot]);
+      const int4 it = item_slot[islot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
       if (++islot == 2) {

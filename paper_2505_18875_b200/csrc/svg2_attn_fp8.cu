@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dv0 = desc_mnmajor_sw128(smem_u32(sV), C::kBlockBytes);
       while (true) {
         mbar_wait_warp(&bars.item_full[islot], iph);
-        const int4 it = read_slot_bcast(&item_slot[islot]);
+        const int4 it = item_slot[islot];
         __syncwarp();
         mbar_arrive_warp(&bars.item_empty[islot]);
         if (++islot == 2) {
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t sph = 0, oph = 0, islot = 0, iph = 0;
     while (true) {
       mbar_wait(&bars.item_full[islot], iph, 18);
-      const int4 it = read_slot_bcast(&item_slot[islot]);
+      const int4 it = item_slot[islot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.item_empty[islot]);
       if (++islot == 2) {
