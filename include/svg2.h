@@ -140,12 +140,15 @@ SVG2_API svg2_status_t svg2_permute(const int32_t* labels, int32_t B, int32_t H,
 
 /* ---- A7, A8: centroid-based top-p selection (Eq. 1, Eq. 2, top-p
  * PAPER.md:314-315).  Per (b,h,i), in fp64: S_ij = scale * sum_k c^q_ik c^k_jk (sequential FMA, k ascending);
- * w_ij = |K_j| exp(S_ij - max_{j:|K_j|>0} S_ij); Z_i = sum_j w_ij (ascending j); sort j by w_ij descending
- * (ties: ascending j) and select ranks while the selected mass < top_p * Z_i (non-empty clusters only);
- * top_p == 1 selects every non-empty key cluster.  mask [B,H,Cq,Ck] out; selected_pairs [B,H] out (nullable). */
+ * w_ij = |K_j| exp(S_ij - max_{j:|K_j|>0} S_ij); Z_i = sum_j w_ij; sort j by w_ij descending (ties: ascending j)
+ * and select the ranks whose preceding mass is < top_p * Z_i (non-empty clusters only); top_p == 1 selects every
+ * non-empty key cluster.  Z_i and the preceding masses are fp64 sums in a fixed tree order (deterministic; equal to
+ * the sequential sums up to rounding, DESIGN R27).  mask [B,H,Cq,Ck] out; selected_pairs [B,H] out (nullable).
+ * ws: svg2_workspace_size(SVG2_ENTRY_SELECT_TOPP, {B,H,*,*,d}, {Cq,Ck,...}) bytes (the fp64 score table). */
 SVG2_API svg2_status_t svg2_select_topp(const float* q_centroids, const float* k_centroids, const int32_t* q_sizes,
-                               const int32_t* k_sizes, int32_t B, int32_t H, int32_t Cq, int32_t Ck, int32_t d,
-                               float scale, double top_p, uint8_t* mask, int64_t* selected_pairs, void* stream);
+                                        const int32_t* k_sizes, int32_t B, int32_t H, int32_t Cq, int32_t Ck,
+                                        int32_t d, float scale, double top_p, uint8_t* mask,
+                                        int64_t* selected_pairs, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- A9 (+ optional A10): dynamic-block-size sparse attention over permuted, cluster-contiguous tokens
  * (PAPER.md:329-334).  For every query row p of cluster i (rows [q_offsets[i], q_offsets[i+1]) of Qp):

@@ -77,7 +77,7 @@ def load_library(path: str = LIB_PATH):
     lib.svg2_kmeans.argtypes = [vp, i32, i32, i32, i32, i32, i32, u32, u32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_permute.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     lib.svg2_select_topp.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, ctypes.c_float, ctypes.c_double, vp,
-                                     vp, vp]
+                                     vp, vp, sz, vp]
     lib.svg2_varblock_attention.argtypes = [vp, vp, vp, Dims, vp, vp, vp, i32, i32, ctypes.c_float, vp, vp, vp, vp,
                                             sz, vp]
     lib.svg2_unpermute.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
@@ -217,8 +217,11 @@ def select_topp(q_centroids, k_centroids, q_sizes, k_sizes, top_p: float, scale:
     Ck = k_centroids.shape[2]
     mask = torch.empty(B, H, Cq, Ck, dtype=torch.uint8, device=q_centroids.device)
     pairs = torch.empty(B, H, dtype=torch.int64, device=q_centroids.device)
+    nbytes = workspace_size(ENTRY_SELECT_TOPP, B, H, 1, 1, d, Cq, Ck)
+    ws = _workspace(max(nbytes, 256), q_centroids.device)
     _check("svg2_select_topp", lib.svg2_select_topp(_p(q_centroids), _p(k_centroids), _p(q_sizes), _p(k_sizes), B, H,
-                                                    Cq, Ck, d, scale, top_p, _p(mask), _p(pairs), _stream()))
+                                                    Cq, Ck, d, scale, top_p, _p(mask), _p(pairs), _p(ws), ws.numel(),
+                                                    _stream()))
     return mask, pairs
 
 

@@ -144,9 +144,11 @@ cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
                           cudaStream_t s, int* launches, const KmeansInit& init = KmeansInit(),
                           const KmeansGather& g = KmeansGather(), double* objective = nullptr);
+// S: fp64 workspace [BH, Cq, Ck] (select_ws_bytes) for the Eq. 1 scores
+inline size_t select_ws_elems(int BH, int Cq, int Ck) { return size_t(BH) * Cq * Ck; }
 cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* sq, const int32_t* sk, int BH,
                                int Cq, int Ck, int d, float scale, double top_p, uint8_t* mask, int64_t* pairs,
-                               cudaStream_t s);
+                               double* S, cudaStream_t s);
 // The attention's output rows, for the NaN fill of query clusters with an empty key stream (k_items)
 struct OrphanFill {
   const int32_t* q_perm;  // nullable: rows in permuted order

@@ -54,6 +54,7 @@ struct FusedWs {
   int32_t *lab_q, *lab_k, *perm_q, *perm_k, *off_q, *off_k, *size_q, *size_k;
   void *Qp, *Kp, *Vp;
   uint8_t* mask;
+  double* scores;    // [BH, Cq, Ck] fp64 Eq. 1 scores of the selection
   uint32_t* v_amax;  // FP8 PV: per-(head, channel) max |V| (f32 bits) [BH, d]
   KmeansWs km_q, km_k;  // per-role k-means scratch: the two roles may run concurrently
   AttnWs attn;
@@ -74,6 +75,7 @@ FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) 
   w.Kp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.Vp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.mask = c.take<uint8_t>(BH * cfg.Cq * cfg.Ck);
+  w.scores = c.take<double>(select_ws_elems(int(BH), cfg.Cq, cfg.Ck));
   w.v_amax = c.take<uint32_t>(BH * dm.d);
   w.km_q = carve_kmeans(c, int(BH), dm.Nq, cfg.Cq);
   w.km_k = carve_kmeans(c, int(BH), dm.Nk, cfg.Ck);
@@ -188,7 +190,7 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   mark(3);
   if (e == cudaSuccess)
     e = launch_select_topp(q_centroids, k_centroids, w.size_q, w.size_k, BH, cfg->Cq, cfg->Ck, dm.d, scale,
-                           cfg->top_p, w.mask, selected_pairs, s);
+                           cfg->top_p, w.mask, selected_pairs, w.scores, s);
   mark(4);
   if (e == cudaSuccess)
     e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck,
@@ -294,6 +296,9 @@ size_t svg2_workspace_size(svg2_entry_t entry, svg2_dims_t dm, const svg2_config
       carve_sort(c, int(BH), dm.Nq, cfg->Cq);
       return c.off + 256;
     case SVG2_ENTRY_SELECT_TOPP:
+      if (BH <= 0 || cfg->Cq < 1 || cfg->Ck < 1 || cfg->Cq > kMaxClusters || cfg->Ck > kMaxClusters) return 0;
+      c.take<double>(select_ws_elems(int(BH), cfg->Cq, cfg->Ck));
+      return c.off + 256;
     case SVG2_ENTRY_UNPERMUTE:
       return 0;
     case SVG2_ENTRY_VARBLOCK_ATTENTION:
@@ -366,16 +371,22 @@ svg2_status_t svg2_permute(const int32_t* labels, int32_t B, int32_t H, int32_t 
 
 svg2_status_t svg2_select_topp(const float* q_centroids, const float* k_centroids, const int32_t* q_sizes,
                                const int32_t* k_sizes, int32_t B, int32_t H, int32_t Cq, int32_t Ck, int32_t d,
-                               float scale, double top_p, uint8_t* mask, int64_t* selected_pairs, void* stream) {
-  if (!q_centroids || !k_centroids || !q_sizes || !k_sizes || !mask) return SVG2_ERR_NULL_POINTER;
+                               float scale, double top_p, uint8_t* mask, int64_t* selected_pairs, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (!q_centroids || !k_centroids || !q_sizes || !k_sizes || !mask || !ws) return SVG2_ERR_NULL_POINTER;
   if (B <= 0 || H <= 0 || (d != 64 && d != 128)) return SVG2_ERR_INVALID_SHAPE;
   if (Cq < 1 || Ck < 1 || Cq > kMaxClusters || Ck > kMaxClusters) return SVG2_ERR_INVALID_PARAM;
   if (!(top_p > 0.0 && top_p <= 1.0) || !(scale >= 0.f) || std::isinf(scale)) return SVG2_ERR_INVALID_PARAM;
+  svg2_config_t cfg{Cq, Ck, 1, top_p, scale, 0u, 0u};
+  svg2_dims_t dm{B, H, 1, 1, d};
+  if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_SELECT_TOPP, dm, &cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
   svg2_status_t st;
   if ((st = check_device()) != SVG2_OK) return st;
   if ((st = pending_error()) != SVG2_OK) return st;
+  Carver c(ws);
+  double* S = c.take<double>(select_ws_elems(B * H, Cq, Ck));
   return from_cuda(launch_select_topp(q_centroids, k_centroids, q_sizes, k_sizes, B * H, Cq, Ck, d,
-                                      resolve_scale(scale, d), top_p, mask, selected_pairs,
+                                      resolve_scale(scale, d), top_p, mask, selected_pairs, S,
                                       static_cast<cudaStream_t>(stream)));
 }
 

@@ -55,7 +55,8 @@ def test_workspace_sizes(lib):
     assert ws < 8 * 2**30
     assert m.workspace_size(m.ENTRY_SPARSE_ATTENTION, 1, 1, 100, 100, 128, 200, 5) == 0  # C > N -> invalid
     assert m.workspace_size(m.ENTRY_SPARSE_ATTENTION, 1, 1, 100, 100, 48, 2, 5) == 0  # d = 48 unsupported
-    assert m.workspace_size(m.ENTRY_SELECT_TOPP, 1, 1, 100, 100, 128, 10, 10) == 0
+    assert m.workspace_size(m.ENTRY_SELECT_TOPP, 1, 1, 100, 100, 128, 10, 10) >= 10 * 10 * 8  # fp64 score table
+    assert m.workspace_size(m.ENTRY_SELECT_TOPP, 1, 1, 100, 100, 128, 10, 5000) == 0  # Ck > 4096
 
 
 def test_validation_rejects_before_touching_the_device(lib):

@@ -224,7 +224,8 @@ def test_fused_call_kmeanspp_cold_start(svg2, oracle_mod):
 
 # ------------------------------------------------------------------ P4: selection
 @pytest.mark.parametrize("p", [0.3, 0.7, 0.9, 0.95, 1.0])
-@pytest.mark.parametrize("Cq,Ck,d", [(16, 32, 64), (100, 500, 128), (37, 1000, 128)])
+@pytest.mark.parametrize("Cq,Ck,d", [(5, 7, 64), (16, 32, 64), (9, 33, 64), (11, 100, 128), (16, 200, 128),
+                                     (100, 500, 128), (37, 1000, 128), (10, 2048, 128), (6, 4000, 128)])
 def test_select_topp_bitexact(svg2, oracle_mod, p, Cq, Ck, d):
     rng = np.random.default_rng(Cq * Ck)
     B, H = 1, 2
