@@ -191,6 +191,38 @@ SVG2_API svg2_status_t svg2_sparse_attention_ex(const void* Q, const void* K, co
                                                 void* O, int64_t* selected_pairs, const svg2_debug_t* dbg,
                                                 void* const* input_ready, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Memory layouts and the multi-GPU split of the fused call (SURVEY 8(b) strides, 8(e), 8(f) row 4).
+ *   q/k/v_strides  element strides (sB, sH, sN) of Q, K, V ([B,H,N,d] logical, d contiguous); {0,0,0} = contiguous.
+ *                  Positive multiples of 8 elements, sN >= d.  E.g. the token-major [B, N, H, d] buffer a Ulysses
+ *                  all-to-all produces is (N*H*d, d, H*d): read in place, no transpose pass.
+ *   o_shards       NULL: O is the call's contiguous [B,H,Nq,d] argument.  Otherwise n_shards (<= 16) device pointers
+ *                  (this process's mappings -- peers' buffers through CUDA IPC or symmetric memory): output token n
+ *                  of head h goes to shard s = n / shard_tokens, row n - s*shard_tokens, at element offset
+ *                  b*o_strides[0] + (h + o_head_offset)*o_strides[1] + row*o_strides[2].  The attention epilogue
+ *                  stores there directly: the inverse permutation (A10) and the reverse Ulysses all-to-all in one
+ *                  store per row.  The O argument is then unused (may be NULL).
+ *   part_begin / part_end / part_count  the query-cluster split of a head across ranks (K/V replicated): every rank
+ *                  runs the same k-means and selection (deterministic, so identical), but the attention covers only
+ *                  the query clusters of parts [part_begin, part_end) of part_count -- per head, cluster i with cost
+ *                  c_i = |Q_i| * keys_i (its selected pairs) and preceding cost P_i belongs to part
+ *                  floor((2 P_i + c_i) part_count / (2 T)), T the head's total -- and writes only their rows.
+ *                  {0, 0, 0} = all clusters.  selected_pairs and the centroid caches are always the whole head's. */
+typedef struct {
+  int64_t q_strides[3], k_strides[3], v_strides[3];
+  void* const* o_shards;
+  int32_t n_shards, shard_tokens, o_head_offset, part_begin;
+  int64_t o_strides[3];
+  int32_t part_end, part_count;
+} svg2_layout_t;
+
+/* The fused call with a layout (NULL layout == svg2_sparse_attention_ex). */
+SVG2_API svg2_status_t svg2_sparse_attention_layout(const void* Q, const void* K, const void* V, svg2_dims_t dims,
+                                                    const svg2_config_t* config, const svg2_layout_t* layout,
+                                                    float* q_centroids, float* k_centroids, void* O,
+                                                    int64_t* selected_pairs, const svg2_debug_t* dbg,
+                                                    void* const* input_ready, void* ws, size_t ws_bytes,
+                                                    void* stream);
+
 /* ---- The fused call on HOST buffers (offload / end-to-end use).  Qh, Kh, Vh [B,H,N,d] bf16 and Oh [B,H,Nq,d] bf16
  * in host memory (page-locked for the copies to overlap; pageable memory works but serialises).  Same math and
  * results as svg2_sparse_attention, bit for bit.  The (b,h) heads are processed in chunks (small first and last ones,

@@ -29,7 +29,8 @@ STATUS = ["SVG2_OK", "SVG2_ERR_NULL_POINTER", "SVG2_ERR_INVALID_SHAPE", "SVG2_ER
           "SVG2_ERR_NOT_IMPLEMENTED"]
 EXPORTED_SYMBOLS = ["svg2_status_string", "svg2_abi_version", "svg2_workspace_size", "svg2_kmeans", "svg2_permute",
                     "svg2_select_topp", "svg2_varblock_attention", "svg2_unpermute", "svg2_sparse_attention",
-                    "svg2_sparse_attention_host", "svg2_sparse_attention_launch_count", "svg2_sparse_attention_ex"]
+                    "svg2_sparse_attention_host", "svg2_sparse_attention_launch_count", "svg2_sparse_attention_ex",
+                    "svg2_sparse_attention_layout"]
 
 
 class SVG2Error(RuntimeError):
@@ -54,6 +55,13 @@ class Debug(ctypes.Structure):
                 ("k_perm", ctypes.c_void_p), ("q_offsets", ctypes.c_void_p), ("k_offsets", ctypes.c_void_p),
                 ("mask", ctypes.c_void_p), ("events", ctypes.c_void_p * 8), ("q_objective", ctypes.c_void_p),
                 ("k_objective", ctypes.c_void_p)]
+
+
+class Layout(ctypes.Structure):
+    _fields_ = [("q_strides", ctypes.c_int64 * 3), ("k_strides", ctypes.c_int64 * 3), ("v_strides", ctypes.c_int64 * 3),
+                ("o_shards", ctypes.c_void_p), ("n_shards", ctypes.c_int32), ("shard_tokens", ctypes.c_int32),
+                ("o_head_offset", ctypes.c_int32), ("part_begin", ctypes.c_int32), ("o_strides", ctypes.c_int64 * 3),
+                ("part_end", ctypes.c_int32), ("part_count", ctypes.c_int32)]
 
 
 _lib = None
@@ -86,10 +94,13 @@ def load_library(path: str = LIB_PATH):
     lib.svg2_sparse_attention_ex.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp,
                                              ctypes.POINTER(Debug), ctypes.POINTER(vp), vp, sz, vp]
     lib.svg2_sparse_attention_host.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), vp, vp, vp, vp, vp, sz, vp]
+    lib.svg2_sparse_attention_layout.argtypes = [vp, vp, vp, Dims, ctypes.POINTER(Config), ctypes.POINTER(Layout), vp,
+                                                 vp, vp, vp, ctypes.POINTER(Debug), ctypes.POINTER(vp), vp, sz, vp]
     lib.svg2_sparse_attention_launch_count.argtypes = [Dims, ctypes.POINTER(Config)]
     lib.svg2_sparse_attention_launch_count.restype = i32
     for name in ["svg2_kmeans", "svg2_permute", "svg2_select_topp", "svg2_varblock_attention", "svg2_unpermute",
-                 "svg2_sparse_attention", "svg2_sparse_attention_ex", "svg2_sparse_attention_host"]:
+                 "svg2_sparse_attention", "svg2_sparse_attention_ex", "svg2_sparse_attention_host",
+                 "svg2_sparse_attention_layout"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -108,12 +119,15 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _need(t, dtype, name, ndim=None):
+def _need(t, dtype, name, ndim=None, strided=False):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name}: expected a CUDA tensor")
     if t.dtype != dtype:
         raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
-    if not t.is_contiguous():
+    if strided:  # [B, H, N, d] view with d contiguous (the library takes element strides sB, sH, sN)
+        if t.stride(-1) != 1:
+            raise ValueError(f"{name}: the last dimension must be contiguous")
+    elif not t.is_contiguous():
         raise ValueError(f"{name}: expected a contiguous tensor")
     if ndim is not None and t.dim() != ndim:
         raise ValueError(f"{name}: expected {ndim} dims, got {tuple(t.shape)}")
@@ -266,16 +280,23 @@ def launch_count(B, H, Nq, Nk, d, Cq, Ck, iters, top_p, warm, init: str = "strid
 
 def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_centroids=None, k_centroids=None,
                      warm: bool = False, scale: float = 0.0, debug: bool = False, events=None, out=None,
-                     init: str = "strided", seed: int = 0, fp8: bool = False, input_ready=None):
+                     init: str = "strided", seed: int = 0, fp8: bool = False, input_ready=None, part=None,
+                     out_shards=None):
     """The fused SVG2 call.  Q, K, V [B,H,N,d] bf16 CUDA.  q_centroids [B,H,Cq,d] / k_centroids [B,H,Ck,d] f32 are
     the centroid caches (read iff warm, always written).  Cold calls start k-means from `init` ("strided" or
     "kmeans++" with `seed`, R25).  Returns (O, selected_pairs, extras) where extras holds
     the centroids and, if debug, the intermediates (labels, perms, offsets, mask).  input_ready: None or three
     torch.cuda.Event recorded when Q, K and V are complete (svg2_sparse_attention_ex): the computation on Q starts
-    while K and V are still arriving."""
+    while K and V are still arriving.
+    Q, K, V may be strided [B,H,N,d] views with d contiguous (e.g. token-major all-to-all buffers viewed as
+    [B,H,N,d]): they are read in place through svg2_sparse_attention_layout.  part = (index, count): compute only
+    that part of every head's query clusters, or (begin, end, count) for parts [begin, end) (multi-GPU split,
+    include/svg2.h).  out_shards = dict(shards=[tensors],
+    shard_tokens=n, strides=(sB, sH, sN), head_offset=h0): write output rows straight into token-sharded buffers
+    (their data pointers; peers' buffers through CUDA IPC), O is then not allocated (None is returned)."""
     lib = load_library()
     for t, n in ((Q, "Q"), (K, "K"), (V, "V")):
-        _need(t, torch.bfloat16, n, 4)
+        _need(t, torch.bfloat16, n, 4, strided=True)
     B, H, Nq, d = Q.shape
     Nk = K.shape[2]
     dev = Q.device
@@ -287,11 +308,34 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
         k_centroids = torch.empty(B, H, Ck, d, dtype=torch.float32, device=dev)
     _need(q_centroids, torch.float32, "q_centroids", 4)
     _need(k_centroids, torch.float32, "k_centroids", 4)
-    O = out if out is not None else torch.empty_like(Q)
+    O = None if out_shards is not None else (out if out is not None else
+                                              torch.empty(B, H, Nq, d, dtype=torch.bfloat16, device=dev))
     pairs = torch.empty(B, H, dtype=torch.int64, device=dev)
     flags = (SVG2_WARM_START if warm else _cold_flags(init)) | (SVG2_FP8_PV if fp8 else 0)
     cfg = Config(Cq, Ck, iters, top_p, scale, flags, seed)
     dims = Dims(B, H, Nq, Nk, d)
+    lay = Layout()
+    keep = []
+    for t, name in ((Q, "q_strides"), (K, "k_strides"), (V, "v_strides")):
+        if not t.is_contiguous():
+            st = [t.stride(0), t.stride(1), t.stride(2)]
+            if t.shape[0] == 1:  # a size-1 dimension's stride is arbitrary in torch: any valid value
+                st[0] = t.shape[1] * t.shape[2] * d
+            if t.shape[1] == 1:
+                st[1] = t.shape[2] * d
+            getattr(lay, name)[:] = st
+    if part is not None:  # (index, count) or (begin, end, count)
+        part = tuple(int(x) for x in part)
+        lay.part_begin, lay.part_end, lay.part_count = (part[0], part[0] + 1, part[1]) if len(part) == 2 else part
+    if out_shards is not None:
+        shards = out_shards["shards"]
+        ptrs = (ctypes.c_void_p * len(shards))(*[int(t.data_ptr()) for t in shards])
+        keep.append(ptrs)
+        lay.o_shards = ctypes.cast(ptrs, ctypes.c_void_p)
+        lay.n_shards = len(shards)
+        lay.shard_tokens = int(out_shards["shard_tokens"])
+        lay.o_strides[:] = [int(x) for x in out_shards["strides"]]
+        lay.o_head_offset = int(out_shards.get("head_offset", 0))
     # 0 = invalid arguments: still call the ABI so the caller gets its precise status code
     nbytes = int(lib.svg2_workspace_size(ENTRY_SPARSE_ATTENTION, dims, ctypes.byref(cfg)))
     ws = _workspace(max(nbytes, 256), dev)
@@ -328,11 +372,11 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
         if not all(ready):
             raise ValueError("input_ready: record every event before the call")
     _check("svg2_sparse_attention",
-           lib.svg2_sparse_attention_ex(_p(Q), _p(K), _p(V), dims, ctypes.byref(cfg), _p(q_centroids),
-                                        _p(k_centroids), _p(O), _p(pairs),
-                                        ctypes.byref(dbg) if dbg is not None else None,
-                                        ctypes.cast(ready, ctypes.POINTER(ctypes.c_void_p)) if ready else None,
-                                        _p(ws), ws.numel(), _stream()))
+           lib.svg2_sparse_attention_layout(_p(Q), _p(K), _p(V), dims, ctypes.byref(cfg), ctypes.byref(lay),
+                                            _p(q_centroids), _p(k_centroids), _p(O), _p(pairs),
+                                            ctypes.byref(dbg) if dbg is not None else None,
+                                            ctypes.cast(ready, ctypes.POINTER(ctypes.c_void_p)) if ready else None,
+                                            _p(ws), ws.numel(), _stream()))
     return O, pairs, extras
 
 

@@ -17,6 +17,57 @@ constexpr int kItemRows = 2 * kQTile;  // one attention work item = two Q tiles 
 constexpr int kItemSplit = 1 << 30;
 constexpr int kItemBhMask = kItemSplit - 1;
 
+// A [B, H, N, d] bf16 tensor (Q, K or V of the fused call) with d contiguous and element strides (sB, sH, sN): head
+// bh = b * H + h, token n.  The contiguous layout is (H N d, N d, d); the token-major buffer of a Ulysses all-to-all
+// [B, N, H, d] is (N H d, d, H d) and is read in place.
+struct XView {
+  const void* p = nullptr;
+  long long sB = 0, sH = 0, sN = 0;
+  int H = 1;
+  __host__ __device__ const uint16_t* row(int bh, long long n) const {
+    return static_cast<const uint16_t*>(p) + (bh / H) * sB + (bh % H) * sH + n * sN;
+  }
+  __host__ __device__ bool contiguous(int N, int d) const { return sN == d && sH == (long long)N * d && sB == H * sH; }
+};
+inline XView contiguous_view(const void* p, int B, int H, int N, int d) {
+  (void)B;
+  XView v;
+  v.p = p;
+  v.sN = d;
+  v.sH = (long long)N * d;
+  v.sB = (long long)H * N * d;
+  v.H = H;
+  return v;
+}
+
+// Where the attention writes output row (bh, token n): the fused A10 scatter, optionally straight into the
+// token-sharded output buffers of a sequence-parallel caller (the reverse Ulysses all-to-all fused into the epilogue:
+// shard s holds tokens [s * shard_tokens, (s + 1) * shard_tokens); peers' shards are IPC / symmetric-memory mappings).
+constexpr int kMaxShards = 16;
+struct OutView {
+  void* shard[kMaxShards] = {};
+  int n_shards = 1;
+  int shard_tokens = 0;
+  long long sB = 0, sH = 0, sN = 0;  // element strides inside a shard
+  int H = 1;                         // heads of the call (bh -> b, h)
+  int head_offset = 0;               // added to h (this call's heads inside the shard's head dimension)
+  __host__ __device__ uint16_t* row(int bh, long long n) const {
+    const int s = n_shards == 1 ? 0 : int(n / shard_tokens);
+    const long long local = n - (long long)s * shard_tokens;
+    return static_cast<uint16_t*>(shard[s]) + (bh / H) * sB + (bh % H + head_offset) * sH + local * sN;
+  }
+};
+inline OutView contiguous_out(void* O, int H, int N, int d) {
+  OutView o;
+  o.shard[0] = O;
+  o.shard_tokens = N;
+  o.sN = d;
+  o.sH = (long long)N * d;
+  o.sB = (long long)H * N * d;
+  o.H = H;
+  return o;
+}
+
 inline int sort_tiles(int N) { return (N + kSortTile - 1) / kSortTile; }
 inline int items_cap_per_bh(int Nq, int Cq) { return (Nq + kItemRows - 1) / kItemRows + Cq; }
 
@@ -99,6 +150,8 @@ struct AttnWs {
   int32_t* items_cnt;  // [BH]
   int4* items;         // [BH * cap] flattened
   int32_t* n_items;    // [3]: item count, dynamic-scheduler counter, query rows with an empty key stream
+  long long* keys;     // [BH, Cq] selected key rows of each query cluster's stream
+  uint8_t* owned;      // [BH, Cq] query cluster belongs to this call's part (QPart)
   size_t gcap, tcap;
 };
 inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Nk, int Cq, int Ck) {
@@ -113,6 +166,8 @@ inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Nk, int Cq, int Ck) {
   w.items_cnt = c.take<int32_t>(BH);
   w.items = c.take<int4>(size_t(BH) * cap);
   w.n_items = c.take<int32_t>(3);
+  w.keys = c.take<long long>(size_t(BH) * Cq);
+  w.owned = c.take<uint8_t>(size_t(BH) * Cq);
   return w;
 }
 
@@ -124,7 +179,7 @@ cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const 
 cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int N, int d, void* O, cudaStream_t s);
 // FP8 PV: per-(head, channel) |x| max (amax [BH, d], f32 bits) and the gather of X[perm] rounded to e4m3 with channel
 // scales 448 / amax_c
-cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, const void* X, void* Xq, uint32_t* amax,
+cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq, uint32_t* amax,
                                     cudaStream_t s);
 // k-means cold-start options (DESIGN R2, R25): strided rows, or k-means++ with the R25 generator
 struct KmeansInit {
@@ -136,11 +191,11 @@ struct KmeansInit {
 // Optional gather fused into the last update pass: Xp = pi X and Yp = pi Y (rows permuted by the final labels).
 struct KmeansGather {
   void* Xp = nullptr;
-  const void* Y = nullptr;
+  XView Y;  // Y.p == nullptr: no second tensor
   void* Yp = nullptr;
   cudaEvent_t wait_y = nullptr;  // Y may still be arriving (host pipeline): the gather pass waits for this event
 };
-cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
+cudaError_t launch_kmeans(XView X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
                           cudaStream_t s, int* launches, const KmeansInit& init = KmeansInit(),
                           const KmeansGather& g = KmeansGather(), double* objective = nullptr);
@@ -151,22 +206,28 @@ cudaError_t launch_select_topp(const float* cq, const float* ck, const int32_t* 
                                double* S, cudaStream_t s);
 // The attention's output rows, for the NaN fill of query clusters with an empty key stream (k_items)
 struct OrphanFill {
-  const int32_t* q_perm;  // nullable: rows in permuted order
-  void* O;                // bf16 [BH, Nq, d]
+  const int32_t* q_perm;  // nullable: rows in permuted order (then out.shard[0] is O [BH, Nq, d])
+  OutView out;
   float* lse;             // nullable
   int d;
+};
+// Query-cluster partition of the attention (multi-GPU split of a head): only the clusters of parts
+// [begin, end) of `count` get work items; parts are cut by the cumulative selected-pair cost |Q_i| * keys_i of the head.
+struct QPart {
+  int begin = 0, end = 1, count = 1;
 };
 // key-stream tile size (8-row groups) the attention pipeline for (d, FP8 PV) runs on: the work list must match it
 int attn_groups_per_tile(int d, bool fp8);
 cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
-                                  int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s);
+                                  int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s,
+                                  QPart part = QPart());
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
-                                      float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
+                                      float scale, const int32_t* q_perm, const OutView& out, float* lse, AttnWs ws,
                                       cudaStream_t s, const uint32_t* v_amax = nullptr);
 int kmeans_launch_count(int iters, bool warm, bool objective = false);
-cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
+cudaError_t launch_kmeanspp(XView X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
                             float* cent, void* ws, cudaStream_t s);
 int kmeanspp_launch_count(int BH, int N, int d);
-constexpr int kSortLaunches = 3, kWorklistLaunches = 2;
+constexpr int kSortLaunches = 3, kWorklistLaunches = 3;
 
 }  // namespace svg2

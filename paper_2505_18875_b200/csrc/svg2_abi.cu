@@ -100,10 +100,11 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
 
 // The whole fused call for the heads of `dm` on stream s (arguments validated by the caller).  bh_base = global
 // (b,h) index of the first head (k-means++ stream ids of chunked calls, R25).
-cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_dims_t& dm, const svg2_config_t* cfg,
-                      float* q_centroids, float* k_centroids, void* O, int64_t* selected_pairs,
+// Q, K, V as strided views, the output rows through `out`, the attention restricted to query-cluster part `part`.
+cudaError_t run_fused(const XView& Q, const XView& K, const XView& V, const svg2_dims_t& dm, const svg2_config_t* cfg,
+                      float* q_centroids, float* k_centroids, const OutView& out, int64_t* selected_pairs,
                       const svg2_debug_t* dbg, FusedWs w, cudaStream_t s, int bh_base,
-                      const cudaEvent_t* arrive = nullptr) {
+                      const cudaEvent_t* arrive = nullptr, QPart part = QPart()) {
   // arrive (host pipeline): events of Q, K and V landing in device memory; each role waits only for its own tensor,
   // V only before the pass that gathers it
   if (dbg) {  // intermediates requested: write them straight into the caller's buffers
@@ -194,10 +195,11 @@ cudaError_t run_fused(const void* Q, const void* K, const void* V, const svg2_di
   mark(4);
   if (e == cudaSuccess)
     e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck,
-                              attn_groups_per_tile(dm.d, fp8), w.attn, OrphanFill{w.perm_q, O, nullptr, dm.d}, s);
+                              attn_groups_per_tile(dm.d, fp8), w.attn, OrphanFill{w.perm_q, out, nullptr, dm.d}, s,
+                              part);
   mark(5);
   if (e == cudaSuccess)
-    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, scale, w.perm_q, O, nullptr, w.attn, s,
+    e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, scale, w.perm_q, out, nullptr, w.attn, s,
                                   fp8 ? w.v_amax : nullptr);
   mark(6);
   mark(7);
@@ -341,7 +343,8 @@ svg2_status_t svg2_kmeans(const void* X, int32_t B, int32_t H, int32_t N, int32_
   init.kmeanspp = (flags & SVG2_INIT_KMEANSPP) != 0;
   init.seed = seed;
   init.role = role;
-  return from_cuda(launch_kmeans(X, B * H, N, d, C, iters, flags & SVG2_WARM_START, centroids, labels, sizes, perm,
+  return from_cuda(launch_kmeans(contiguous_view(X, B, H, N, d), B * H, N, d, C, iters, flags & SVG2_WARM_START,
+                                 centroids, labels, sizes, perm,
                                  offsets, kw, static_cast<cudaStream_t>(stream), nullptr, init, KmeansGather(),
                                  objective));
 }
@@ -411,10 +414,11 @@ svg2_status_t svg2_varblock_attention(const void* Qp, const void* Kp, const void
   AttnWs aw = carve_attn(c, BH, dm.Nq, dm.Nk, Cq, Ck);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = launch_build_worklist(q_offsets, k_offsets, mask, BH, dm.Nq, dm.Nk, Cq, Ck,
-                                        attn_groups_per_tile(dm.d, false), aw, OrphanFill{q_perm, O, lse, dm.d}, s);
+                                        attn_groups_per_tile(dm.d, false), aw,
+                                        OrphanFill{q_perm, contiguous_out(O, dm.H, dm.Nq, dm.d), lse, dm.d}, s);
   if (e == cudaSuccess)
-    e = launch_varblock_attention(Qp, Kp, Vp, BH, dm.Nq, dm.Nk, dm.d, resolve_scale(scale, dm.d), q_perm, O, lse,
-                                  aw, s);
+    e = launch_varblock_attention(Qp, Kp, Vp, BH, dm.Nq, dm.Nk, dm.d, resolve_scale(scale, dm.d), q_perm,
+                                  contiguous_out(O, dm.H, dm.Nq, dm.d), lse, aw, s);
   return from_cuda(e);
 }
 
@@ -453,13 +457,73 @@ svg2_status_t svg2_sparse_attention_ex(const void* Q, const void* K, const void*
                                        const svg2_config_t* cfg, float* q_centroids, float* k_centroids, void* O,
                                        int64_t* selected_pairs, const svg2_debug_t* dbg, void* const* input_ready,
                                        void* ws, size_t ws_bytes, void* stream) {
+  return svg2_sparse_attention_layout(Q, K, V, dm, cfg, nullptr, q_centroids, k_centroids, O, selected_pairs, dbg,
+                                      input_ready, ws, ws_bytes, stream);
+}
+
+namespace {
+bool strides_ok(const int64_t* st, int d) {  // (sB, sH, sN): positive multiples of 8 elements (16-byte TMA rows)
+  for (int i = 0; i < 3; ++i)
+    if (st[i] <= 0 || st[i] % 8) return false;
+  return st[2] >= d;
+}
+XView view_of(const void* p, const svg2_dims_t& dm, int N, const int64_t* st) {
+  if (!st || (st[0] == 0 && st[1] == 0 && st[2] == 0)) return contiguous_view(p, dm.B, dm.H, N, dm.d);
+  XView v;
+  v.p = p;
+  v.sB = st[0];
+  v.sH = st[1];
+  v.sN = st[2];
+  v.H = dm.H;
+  return v;
+}
+bool zero3(const int64_t* st) { return st[0] == 0 && st[1] == 0 && st[2] == 0; }
+}  // namespace
+
+svg2_status_t svg2_sparse_attention_layout(const void* Q, const void* K, const void* V, svg2_dims_t dm,
+                                           const svg2_config_t* cfg, const svg2_layout_t* lay, float* q_centroids,
+                                           float* k_centroids, void* O, int64_t* selected_pairs,
+                                           const svg2_debug_t* dbg, void* const* input_ready, void* ws,
+                                           size_t ws_bytes, void* stream) {
   if (input_ready && (!input_ready[0] || !input_ready[1] || !input_ready[2])) return SVG2_ERR_NULL_POINTER;
-  if (!Q || !K || !V || !cfg || !q_centroids || !k_centroids || !O || !ws) return SVG2_ERR_NULL_POINTER;
+  const bool sharded = lay && lay->o_shards;
+  if (!Q || !K || !V || !cfg || !q_centroids || !k_centroids || (!O && !sharded) || !ws) return SVG2_ERR_NULL_POINTER;
   svg2_status_t st = validate_fused(dm, cfg);
   if (st != SVG2_OK) return st;
-  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(q_centroids) ||
+  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || (!sharded && !aligned16(O)) || !aligned16(q_centroids) ||
       !aligned16(k_centroids))
     return SVG2_ERR_MISALIGNED;
+  QPart part;
+  OutView out = contiguous_out(O, dm.H, dm.Nq, dm.d);
+  if (lay) {
+    const int64_t* strs[3] = {lay->q_strides, lay->k_strides, lay->v_strides};
+    for (int t = 0; t < 3; ++t)
+      if (!zero3(strs[t]) && !strides_ok(strs[t], dm.d)) return SVG2_ERR_INVALID_SHAPE;
+    if (lay->part_count != 0 || lay->part_begin != 0 || lay->part_end != 0) {
+      if (lay->part_count < 1 || lay->part_count > kMaxClusters || lay->part_begin < 0 ||
+          lay->part_end <= lay->part_begin || lay->part_end > lay->part_count)
+        return SVG2_ERR_INVALID_PARAM;
+      part.begin = lay->part_begin;
+      part.end = lay->part_end;
+      part.count = lay->part_count;
+    }
+    if (sharded) {
+      if (lay->n_shards < 1 || lay->n_shards > kMaxShards || lay->shard_tokens < 1 ||
+          (long long)lay->n_shards * lay->shard_tokens < dm.Nq || lay->o_head_offset < 0 || !strides_ok(lay->o_strides, dm.d))
+        return SVG2_ERR_INVALID_SHAPE;
+      out.n_shards = lay->n_shards;
+      out.shard_tokens = lay->shard_tokens;
+      for (int i = 0; i < lay->n_shards; ++i) {
+        if (!lay->o_shards[i]) return SVG2_ERR_NULL_POINTER;
+        if (!aligned16(lay->o_shards[i])) return SVG2_ERR_MISALIGNED;
+        out.shard[i] = lay->o_shards[i];
+      }
+      out.sB = lay->o_strides[0];
+      out.sH = lay->o_strides[1];
+      out.sN = lay->o_strides[2];
+      out.head_offset = lay->o_head_offset;
+    }
+  }
   if (ws_bytes < svg2_workspace_size(SVG2_ENTRY_SPARSE_ATTENTION, dm, cfg)) return SVG2_ERR_WORKSPACE_TOO_SMALL;
   if ((st = check_device()) != SVG2_OK) return st;
   if ((st = pending_error()) != SVG2_OK) return st;
@@ -469,8 +533,11 @@ svg2_status_t svg2_sparse_attention_ex(const void* Q, const void* K, const void*
   cudaEvent_t ready[3];
   if (input_ready)
     for (int i = 0; i < 3; ++i) ready[i] = static_cast<cudaEvent_t>(input_ready[i]);
-  return from_cuda(run_fused(Q, K, V, dm, cfg, q_centroids, k_centroids, O, selected_pairs, dbg, w,
-                             static_cast<cudaStream_t>(stream), 0, input_ready ? ready : nullptr));
+  const XView qv = view_of(Q, dm, dm.Nq, lay ? lay->q_strides : nullptr);
+  const XView kv = view_of(K, dm, dm.Nk, lay ? lay->k_strides : nullptr);
+  const XView vv = view_of(V, dm, dm.Nk, lay ? lay->v_strides : nullptr);
+  return from_cuda(run_fused(qv, kv, vv, dm, cfg, q_centroids, k_centroids, out, selected_pairs, dbg, w,
+                             static_cast<cudaStream_t>(stream), 0, input_ready ? ready : nullptr, part));
 }
 
 svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const void* Vh, svg2_dims_t dm,
@@ -530,8 +597,9 @@ svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const v
     if (e == cudaSuccess) {
       const svg2_dims_t cd{1, nh, dm.Nq, dm.Nk, dm.d};
       const cudaEvent_t arrive[3] = {evqk[2 * ci], evqk[2 * ci + 1], in};  // the computation starts on Q alone
-      e = run_fused(w.Q[slot], w.K[slot], w.V[slot], cd, cfg, q_centroids + size_t(bh0) * cfg->Cq * dm.d,
-                    k_centroids + size_t(bh0) * cfg->Ck * dm.d, w.O[slot],
+      e = run_fused(contiguous_view(w.Q[slot], 1, nh, dm.Nq, dm.d), contiguous_view(w.K[slot], 1, nh, dm.Nk, dm.d),
+                    contiguous_view(w.V[slot], 1, nh, dm.Nk, dm.d), cd, cfg, q_centroids + size_t(bh0) * cfg->Cq * dm.d,
+                    k_centroids + size_t(bh0) * cfg->Ck * dm.d, contiguous_out(w.O[slot], nh, dm.Nq, dm.d),
                     selected_pairs ? selected_pairs + bh0 : nullptr, nullptr, w.fused[cs], sc, bh0,
                     arrive);
     }

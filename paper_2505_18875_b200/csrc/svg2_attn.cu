@@ -112,7 +112,8 @@ struct Params {
   const int32_t* ngroups;
   size_t gcap, tcap;
   const int32_t* q_perm;
-  __nv_bfloat16* O;
+  __nv_bfloat16* O;  // permuted-order output (q_perm == nullptr)
+  OutView out;       // original-order output rows (q_perm set): the fused A10 scatter
   float* lse;
   int Nq;
   float scale_log2;
@@ -570,8 +571,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float ca = wa / lt, cb = wb / lt;
         const long long row_flat = (long long)it.x + rloc;
         long long dst = row_flat;
-        if (rloc < nrows && p.q_perm) dst = (long long)(it.w & kItemBhMask) * p.Nq + __ldg(p.q_perm + row_flat);
         uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);
+        if (rloc < nrows && p.q_perm) {
+          const int bh = it.w & kItemBhMask;
+          const int n = __ldg(p.q_perm + row_flat);
+          dst = (long long)bh * p.Nq + n;
+          orow = reinterpret_cast<uint4*>(p.out.row(bh, n));
+        }
         const uint32_t tOb = tmem + lane_addr + C::col_o(1);
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
@@ -603,11 +609,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l;
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
-      if (rloc < nrows && p.q_perm) {
-        const long long bh = it.w & kItemBhMask;
-        dst = bh * p.Nq + __ldg(p.q_perm + row_flat);
-      }
       uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);
+      if (rloc < nrows && p.q_perm) {
+        const int bh = it.w & kItemBhMask;
+        const int n = __ldg(p.q_perm + row_flat);
+        dst = (long long)bh * p.Nq + n;
+        orow = reinterpret_cast<uint4*>(p.out.row(bh, n));
+      }
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
@@ -638,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D>
 cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
-                     const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s) {
+                     const int32_t* q_perm, const OutView& out, float* lse, AttnWs ws, cudaStream_t s) {
   using C = Cfg<D>;
   CUtensorMap mq;
   KVMaps kv;
@@ -656,7 +664,8 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
   p.gcap = ws.gcap;
   p.tcap = ws.tcap;
   p.q_perm = q_perm;
-  p.O = static_cast<__nv_bfloat16*>(O);
+  p.O = static_cast<__nv_bfloat16*>(out.shard[0]);
+  p.out = out;
   p.lse = lse;
   p.Nq = Nq;
   p.scale_log2 = scale * 1.4426950408889634f;
@@ -711,8 +720,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   const size_t li = size_t(bh) * Cq + i;
   const uint8_t* mrow = mask + li * Ck;
   const int32_t* ko = k_off + size_t(bh) * (Ck + 1);
-  // 1) compact the selected, non-empty clusters (ascending j)
-  int base = 0;
+  // 1) compact the selected, non-empty clusters (ascending j); count the stream's key rows
+  int base = 0, nkeys = 0;
   for (int j0 = 0; j0 < Ck; j0 += kBuildThreads) {
     const int j = j0 + tid;
     int s = 0, e = 0, f = 0;
@@ -721,14 +730,17 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
       e = __ldg(ko + j + 1);
       f = e > s;
     }
-    int tot;
+    int tot, rows;
     const int pos = base + build_scan(f, &tot);
     if (f) {
       sel_s[pos] = s;
       sel_e[pos] = e;
     }
     base += tot;
+    build_scan(e - s, &rows);
+    nkeys += rows;
   }
+  if (tid == 0) ws.keys[li] = nkeys;
   const int nsel = base;
   __syncthreads();
   // 2) runs: a selected cluster starts a run unless it begins exactly where the previous one ends
@@ -806,6 +818,49 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   }
 }
 
+// Query-cluster partition (QPart): per head, cluster i costs c_i = |Q_i| * keys_i (its attention pairs); with P_i the
+// cost of clusters 0..i-1 and T the head's total, cluster i belongs to part floor((2 P_i + c_i) * count / (2 T)) --
+// the part its cost midpoint falls in, so the parts' costs differ by at most one cluster; owned = part in
+// [begin, end).  One CTA per head.
+__global__ void __launch_bounds__(1024) k_parts(const int32_t* __restrict__ q_off, int Cq, QPart part, AttnWs ws) {
+  __shared__ long long wsum[32];
+  const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  constexpr int kPer = (kMaxClusters + 1023) / 1024;  // clusters per thread (contiguous)
+  long long c[kPer], run = 0;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = tid * kPer + u;
+    c[u] = 0;
+    if (i < Cq) {
+      const long long sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q_off[size_t(bh) * (Cq + 1) + i];
+      c[u] = sq * ws.keys[size_t(bh) * Cq + i];
+    }
+    run += c[u];
+  }
+  long long x = run;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  long long before = 0, T = 0;
+  for (int k = 0; k < 32; ++k) {
+    before += k < w ? wsum[k] : 0;
+    T += wsum[k];
+  }
+  long long P = before + x - run;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = tid * kPer + u;
+    if (i < Cq) {
+      const long long pi = T > 0 ? (2 * P + c[u]) * part.count / (2 * T) : 0;
+      ws.owned[size_t(bh) * Cq + i] = pi >= part.begin && pi < part.end;
+    }
+    P += c[u];
+  }
+}
+
 // Work items in (b,h)-major, cluster order: ceil(|Q_i| / 256) pairs of 128-row Q tiles per non-empty query cluster
 // with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.  A
 // query cluster whose mask row selects no non-empty key cluster (a contract violation of svg2_varblock_attention,
@@ -829,7 +884,9 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
       const int i = c - bh * Cq;
       q0 = q_off[size_t(bh) * (Cq + 1) + i];
       sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q0;
-      if (ws.ngroups[c] > 0) {
+      if (!ws.owned[c]) {
+        // another part's query cluster (multi-GPU split of the head): no items, no output rows here
+      } else if (ws.ngroups[c] > 0) {
         n = (sq + kItemRows - 1) / kItemRows;
       } else if (sq > 0) {
         atomicAdd(&n_orphan, sq);
@@ -837,7 +894,8 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
         for (int r = 0; r < sq; ++r) {
           const long long row_flat = (long long)bh * Nq + q0 + r;
           const long long dst = of.q_perm ? (long long)bh * Nq + of.q_perm[row_flat] : row_flat;
-          uint4* orow = reinterpret_cast<uint4*>(static_cast<uint16_t*>(of.O) + dst * of.d);
+          uint4* orow = reinterpret_cast<uint4*>(of.q_perm ? of.out.row(bh, of.q_perm[row_flat])
+                                                           : static_cast<uint16_t*>(of.out.shard[0]) + dst * of.d);
           for (int v = 0; v < of.d / 8; ++v) orow[v] = nan4;
           if (of.lse) of.lse[dst] = __int_as_float(0x7FC00000);
         }
@@ -880,25 +938,27 @@ static_assert(Cfg<128>::kGpt >= kMinGroupsPerTile && Cfg<64>::kGpt >= kMinGroups
 int attn_groups_per_tile(int d, bool fp8) { return fp8 ? kKTile / 8 : (d == 128 ? Cfg<128>::kGpt : Cfg<64>::kGpt); }
 
 cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
-                                  int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s) {
+                                  int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s,
+                                  QPart part) {
   const size_t smem = (5 * size_t(Ck) + 1) * sizeof(int);
   cudaFuncSetAttribute(k_build_streams, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k_build_streams<<<dim3(Cq, BH), kBuildThreads, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, gpt, ws);
+  k_parts<<<BH, 1024, 0, s>>>(q_offsets, Cq, part, ws);
   k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, gpt, ws, of);
   return cudaGetLastError();
 }
 
 // svg2_attn_fp8.cu: the FP8 PV pipeline (DESIGN R26), 128-key tiles
 cudaError_t launch_varblock_attention_fp8(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk,
-                                          int d, float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
-                                          cudaStream_t s, const uint32_t* v_amax);
+                                          int d, float scale, const int32_t* q_perm, const OutView& out, float* lse,
+                                          AttnWs ws, cudaStream_t s, const uint32_t* v_amax);
 
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
-                                      float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
+                                      float scale, const int32_t* q_perm, const OutView& out, float* lse, AttnWs ws,
                                       cudaStream_t s, const uint32_t* v_amax) {
-  if (v_amax) return launch_varblock_attention_fp8(Qp, Kp, Vp, BH, Nq, Nk, d, scale, q_perm, O, lse, ws, s, v_amax);
-  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s);
-  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s);
+  if (v_amax) return launch_varblock_attention_fp8(Qp, Kp, Vp, BH, Nq, Nk, d, scale, q_perm, out, lse, ws, s, v_amax);
+  if (d == 128) return run_attn<128>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, out, lse, ws, s);
+  return run_attn<64>(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, out, lse, ws, s);
 }
 
 }  // namespace svg2

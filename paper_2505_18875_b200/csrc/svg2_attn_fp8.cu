@@ -86,7 +86,8 @@ struct Params {
   const int32_t* ngroups;
   size_t gcap, tcap;
   const int32_t* q_perm;
-  __nv_bfloat16* O;
+  __nv_bfloat16* O;  // permuted-order output (q_perm == nullptr)
+  OutView out;       // original-order output rows (q_perm set): the fused A10 scatter
   float* lse;
   int Nq;
   float scale_log2;
@@ -546,8 +547,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t* vam = kFp8 ? p.v_amax + size_t(it.w & kItemBhMask) * D : nullptr;
         const long long row_flat = (long long)it.x + rloc;
         long long dst = row_flat;
-        if (rloc < nrows && p.q_perm) dst = (long long)(it.w & kItemBhMask) * p.Nq + __ldg(p.q_perm + row_flat);
         uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);
+        if (rloc < nrows && p.q_perm) {
+          const int bh = it.w & kItemBhMask;
+          const int n = __ldg(p.q_perm + row_flat);
+          dst = (long long)bh * p.Nq + n;
+          orow = reinterpret_cast<uint4*>(p.out.row(bh, n));
+        }
         const uint32_t tOb = tmem + lane_addr + C::col_o(1);
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
@@ -582,11 +588,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t* vam = kFp8 ? p.v_amax + size_t(it.w & kItemBhMask) * D : nullptr;
       const long long row_flat = (long long)it.x + g * kQTile + rloc;
       long long dst = row_flat;
-      if (rloc < nrows && p.q_perm) {
-        const long long bh = it.w & kItemBhMask;
-        dst = bh * p.Nq + __ldg(p.q_perm + row_flat);
-      }
       uint4* orow = reinterpret_cast<uint4*>(p.O + dst * D);
+      if (rloc < nrows && p.q_perm) {
+        const int bh = it.w & kItemBhMask;
+        const int n = __ldg(p.q_perm + row_flat);
+        dst = (long long)bh * p.Nq + n;
+        orow = reinterpret_cast<uint4*>(p.out.row(bh, n));
+      }
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
@@ -622,7 +630,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 cudaError_t run_attn_fp8(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, float scale,
-                         const int32_t* q_perm, void* O, float* lse, AttnWs ws, cudaStream_t s, const uint32_t* v_amax) {
+                         const int32_t* q_perm, const OutView& out, float* lse, AttnWs ws, cudaStream_t s,
+                         const uint32_t* v_amax) {
   constexpr int D = 128;
   CUtensorMap mq;
   KVMaps kv;
@@ -640,7 +649,8 @@ cudaError_t run_attn_fp8(const void* Qp, const void* Kp, const void* Vp, int BH,
   p.gcap = ws.gcap;
   p.tcap = ws.tcap;
   p.q_perm = q_perm;
-  p.O = static_cast<__nv_bfloat16*>(O);
+  p.O = static_cast<__nv_bfloat16*>(out.shard[0]);
+  p.out = out;
   p.lse = lse;
   p.Nq = Nq;
   p.scale_log2 = scale * 1.4426950408889634f;
@@ -657,10 +667,10 @@ cudaError_t run_attn_fp8(const void* Qp, const void* Kp, const void* Vp, int BH,
 }  // namespace
 
 cudaError_t launch_varblock_attention_fp8(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk,
-                                          int d, float scale, const int32_t* q_perm, void* O, float* lse, AttnWs ws,
-                                          cudaStream_t s, const uint32_t* v_amax) {
+                                          int d, float scale, const int32_t* q_perm, const OutView& out, float* lse,
+                                          AttnWs ws, cudaStream_t s, const uint32_t* v_amax) {
   if (d != 128 || !v_amax) return cudaErrorNotSupported;
-  return run_attn_fp8(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, O, lse, ws, s, v_amax);
+  return run_attn_fp8(Qp, Kp, Vp, BH, Nq, Nk, scale, q_perm, out, lse, ws, s, v_amax);
 }
 
 }  // namespace svg2

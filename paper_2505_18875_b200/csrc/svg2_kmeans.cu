@@ -70,7 +70,7 @@ template <int D>
 __global__ void __launch_bounds__(kAsgThreads, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
                 const __grid_constant__ CUtensorMap mapLo, const float* __restrict__ c_norm, int N, int Cpad,
-                int BH, int32_t* __restrict__ labels) {
+                int BH, int H, int32_t* __restrict__ labels) {
   using C = AsgCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         mbar_wait(&bars.x_empty[xs], ((i >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars.x_full[xs], C::kTileBytes);
         for (int b = 0; b < C::kBlocks; ++b)
-          tma_load_2d(sX + xs * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full[xs], 64 * b, bh * N + row0);
+          tma_load_4d(sX + xs * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full[xs], 64 * b, row0, bh % H,
+                      bh / H);
         for (int c = 0; c < nchunks; ++c, ++cc) {
           const int s = cc & 1;
           mbar_wait(&bars.c_empty[s], ((cc >> 1) & 1) ^ 1);
@@ -256,7 +257,7 @@ constexpr int kSumRows = 64, kSumUnroll = 8, kSumWarps = 4;
 // Plain update (no gather): rows gathered through perm into registers, kSumUnroll loads in flight per warp (lane l
 // holds D/32 consecutive columns, so one row is one coalesced D*2-byte read).
 template <int D>
-__global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat16* __restrict__ X, int N, int C,
+__global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, int N, int C,
                                                              const int32_t* __restrict__ perm,
                                                              const int32_t* __restrict__ offsets, SegOut out) {
   constexpr int kCols = D / 32;  // 4 (d = 128) or 2 (d = 64) bf16 per lane
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
     if (__ldg(off + mid) <= p0) lo = mid; else hi = mid - 1;
   }
   int j = lo, next = __ldg(off + j + 1);
-  const Vec* Xv = reinterpret_cast<const Vec*>(X) + size_t(bh) * N * 32;  // 32 Vec per row
+  const uint16_t* xb = X.row(bh, 0);
   const int32_t* pm = perm + size_t(bh) * N;
   double acc[kCols], sq = 0.0;
 #pragma unroll
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
 #pragma unroll
     for (int u = 0; u < kSumUnroll; ++u) {
       const int src = __shfl_sync(0xffffffffu, src_l, u);
-      if (pb + u < p1) v[u] = __ldg(Xv + size_t(src) * 32 + lane);
+      if (pb + u < p1) v[u] = __ldg(reinterpret_cast<const Vec*>(xb + src * X.sN) + lane);
     }
 #pragma unroll
     for (int u = 0; u < kSumUnroll; ++u) {
@@ -326,9 +327,8 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const __nv_bfloat
 constexpr int kAsyncWarps = 4, kAsyncRows = kUpdMinRows;
 template <int D>
 __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
-    const __nv_bfloat16* __restrict__ X, int N, int C, const int32_t* __restrict__ perm,
-    const int32_t* __restrict__ offsets, SegOut out, __nv_bfloat16* __restrict__ Xp,
-    const __nv_bfloat16* __restrict__ Y, __nv_bfloat16* __restrict__ Yp) {
+    const XView X, int N, int C, const int32_t* __restrict__ perm, const int32_t* __restrict__ offsets, SegOut out,
+    __nv_bfloat16* __restrict__ Xp, const XView Y, __nv_bfloat16* __restrict__ Yp) {
   constexpr int kCols = D / 32;           // bf16 per lane in the accumulation
   constexpr int kRowBytes = D * 2;        // 256 (d = 128) or 128 (d = 64)
   constexpr int kVecPerRow = kRowBytes / 16;
@@ -341,11 +341,12 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   const int p0 = chunk * kRows;
   if (p0 >= N) return;
   const int nrow = min(N - p0, kRows);
-  const bool with_y = Y != nullptr, want_sq = out.sq != nullptr;
+  const bool with_y = Y.p != nullptr, want_sq = out.sq != nullptr;
   const int32_t* pm = perm + size_t(bh) * N + p0;
   const int src0 = lane < nrow ? __ldg(pm + lane) : 0;
-  const uint8_t* xb = reinterpret_cast<const uint8_t*>(X) + size_t(bh) * N * kRowBytes;
-  const uint8_t* yb = with_y ? reinterpret_cast<const uint8_t*>(Y) + size_t(bh) * N * kRowBytes : nullptr;
+  const uint8_t* xb = reinterpret_cast<const uint8_t*>(X.row(bh, 0));
+  const uint8_t* yb = with_y ? reinterpret_cast<const uint8_t*>(Y.row(bh, 0)) : nullptr;
+  const long long xrow = X.sN * 2, yrow = Y.sN * 2;  // bytes between tokens
   // issue: 32 lanes cover 32 / kVecPerRow rows per step, one 16-byte piece each
   constexpr int kRowsPerStep = 32 / kVecPerRow;
   const int piece = lane % kVecPerRow, rsub = lane / kVecPerRow;
@@ -354,11 +355,11 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
     const int src = __shfl_sync(0xffffffffu, src0, r & 31);
     if (r < nrow) {
       const uint32_t dst = smem_u32(sx + r * kRowBytes + piece * 16);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(xb + size_t(src) * kRowBytes + piece * 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(xb + src * xrow + piece * 16)
                    : "memory");
       if (with_y) {
         const uint32_t dy = smem_u32(sy + r * kRowBytes + piece * 16);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dy), "l"(yb + size_t(src) * kRowBytes + piece * 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dy), "l"(yb + src * yrow + piece * 16)
                      : "memory");
       }
     }
@@ -494,21 +495,22 @@ __global__ void k_objective(int BH, int C, const double* __restrict__ jpart, dou
 }
 
 template <int D>
-__global__ void k_init_cold(const __nv_bfloat16* __restrict__ X, int N, int C, float* __restrict__ cent) {
+__global__ void k_init_cold(const XView X, int N, int C, float* __restrict__ cent) {
   const int j = blockIdx.x, bh = blockIdx.y;
   const long long src = (long long)j * N / C;  // floor(j N / C)
-  cent[(size_t(bh) * C + j) * D + threadIdx.x] = __bfloat162float(X[(size_t(bh) * N + src) * D + threadIdx.x]);
+  const uint16_t bits = X.row(bh, src)[threadIdx.x];
+  cent[(size_t(bh) * C + j) * D + threadIdx.x] = __uint_as_float(uint32_t(bits) << 16);
 }
 
 template <int D>
-cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool warm, const KmeansInit& init,
+cudaError_t run_kmeans(const XView X, int BH, int N, int C, int iters, bool warm, const KmeansInit& init,
                        float* cent, int32_t* labels,
                        int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws, cudaStream_t s,
                        const KmeansGather& g, double* objective) {
-  const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(Xv);
   const int Cpad = cent_pad(C);
   CUtensorMap mx, mh, ml;
-  if (!make_tmap_bf16(&mx, Xv, uint64_t(BH) * N, D, 128) || !make_tmap_bf16(&mh, ws.c_hi, uint64_t(BH) * Cpad, D, 128) ||
+  if (!make_tmap_bf16_4d(&mx, X.p, D, N, X.H, BH / X.H, X.sN, X.sH, X.sB, 128) ||
+      !make_tmap_bf16(&mh, ws.c_hi, uint64_t(BH) * Cpad, D, 128) ||
       !make_tmap_bf16(&ml, ws.c_lo, uint64_t(BH) * Cpad, D, 128))
     return cudaErrorInvalidValue;
   cudaFuncSetAttribute(k_assign_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<D>::kSmem);
@@ -518,7 +520,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
   const long long units = (long long)BH * ((N + kAsgRows - 1) / kAsgRows);
   const int grid_asg = int(units < sms ? units : sms);  // persistent: one CTA per SM
   if (!warm && init.kmeanspp) {
-    cudaError_t e = launch_kmeanspp(Xv, BH, N, D, C, init.seed, init.role, init.bh_base, cent, ws.pp, s);
+    cudaError_t e = launch_kmeanspp(X, BH, N, D, C, init.seed, init.role, init.bh_base, cent, ws.pp, s);
     if (e != cudaSuccess) return e;
   } else if (!warm) {
     k_init_cold<D><<<dim3(C, BH), D, 0, s>>>(X, N, C, cent);
@@ -527,7 +529,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
   __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
   for (int it = 0; it < iters; ++it) {
     k_centroid_split<D><<<dim3(Cpad, BH), D, 0, s>>>(cent, C, Cpad, hi, lo, ws.c_norm);
-    k_assign_tc<D><<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, labels);
+    k_assign_tc<D><<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, X.H, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
     // the gather pass (last iteration) uses the asynchronous-copy kernel: K' + V' 0.69 -> 0.48 ms, Q' equal; the
@@ -541,8 +543,7 @@ cudaError_t run_kmeans(const void* Xv, int BH, int N, int C, int iters, bool war
       const size_t sm = size_t(kAsyncWarps) * 2 * kAsyncRows * D * 2;
       cudaFuncSetAttribute(k_update_sum_async<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
       k_update_sum_async<D><<<grid_a, 32 * kAsyncWarps, sm, s>>>(
-          X, N, C, perm, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp), static_cast<const __nv_bfloat16*>(g.Y),
-          static_cast<__nv_bfloat16*>(g.Yp));
+          X, N, C, perm, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp), g.Y, static_cast<__nv_bfloat16*>(g.Yp));
     } else {
       const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
       k_update_sum<D><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, seg);
@@ -560,7 +561,7 @@ int kmeans_launch_count(int iters, bool warm, bool objective) {
   return (warm ? 0 : 1) + iters * (4 + kSortLaunches + (objective ? 1 : 0));
 }
 
-cudaError_t launch_kmeans(const void* X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
+cudaError_t launch_kmeans(XView X, int BH, int N, int d, int C, int iters, bool warm, float* centroids,
                           int32_t* labels, int32_t* sizes, int32_t* perm, int32_t* offsets, KmeansWs ws,
                           cudaStream_t s, int* launches, const KmeansInit& init, const KmeansGather& g,
                           double* objective) {

@@ -71,7 +71,7 @@ struct PPWs {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __restrict__ X, int N, int C, int bh0,
+__global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const XView X, int N, int C, int bh0,
                                                         int nblk, uint32_t seed, uint32_t stream_base,
                                                         float* __restrict__ cent, PPWs ws) {
   cg::grid_group grid = cg::this_grid();
@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
   __shared__ double red[kPPThreads / 32];
   __shared__ unsigned long long part_s[kPPMaxBlocks];
   double* Dv = ws.D + size_t(bh) * N;
-  const __nv_bfloat16* Xb = X + size_t(bh) * N * D;
+  const __nv_bfloat16* Xb = reinterpret_cast<const __nv_bfloat16*>(X.row(bh, 0));
+  const long long sN = X.sN;
   const uint32_t stream = 2u * uint32_t(bh) + stream_base;  // 2 * (global bh) + role
   double dref = 0.0;
   for (int j = 0; j < C; ++j) {
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
       pick = *((volatile int32_t*)(ws.pick + bh));
     }
     for (int k = tid; k < D; k += kPPThreads) {
-      const float v = __bfloat162float(Xb[size_t(pick) * D + k]);
+      const float v = __bfloat162float(Xb[pick * sN + k]);
       c_s[k] = double(v);
       if (blk == 0) cent[(size_t(bh) * C + j) * D + k] = v;  // a data row: exact in f32
     }
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kPPThreads) k_kmeanspp(const __nv_bfloat16* __
     unsigned long long wsum = 0;
     double tmax = 0.0;
     for (int n = t0; n < t1; ++n) {
-      double dn = sqdist_rn<D>(Xb + size_t(n) * D, c_s);
+      double dn = sqdist_rn<D>(Xb + n * sN, c_s);
       if (j > 0) {
         const double old = Dv[n];
         dn = dn < old ? dn : old;
@@ -232,7 +233,7 @@ PPPlan pp_plan(int BH, int N) {
 }
 }  // namespace
 
-cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
+cudaError_t launch_kmeanspp(XView X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
                             float* cent, void* ws_ptr, cudaStream_t s) {
   uint32_t stream_base = 2u * uint32_t(bh_base) + uint32_t(role);
   auto run = [&](auto kernel, PPPlan plan) -> cudaError_t {
@@ -245,11 +246,10 @@ cudaError_t launch_kmeanspp(const void* X, int BH, int N, int d, int C, uint32_t
     w.part = reinterpret_cast<unsigned long long*>(base);
     base += size_t(BH) * kPPMaxBlocks * sizeof(unsigned long long);
     w.pick = reinterpret_cast<int32_t*>(base);
-    const __nv_bfloat16* Xb = static_cast<const __nv_bfloat16*>(X);
     int nblk = plan.nblk;
     for (int bh0 = 0; bh0 < BH; bh0 += plan.heads_per_launch) {
       const int nh = BH - bh0 < plan.heads_per_launch ? BH - bh0 : plan.heads_per_launch;
-      void* args[] = {(void*)&Xb, (void*)&N, (void*)&C, (void*)&bh0, (void*)&nblk, (void*)&seed,
+      void* args[] = {(void*)&X, (void*)&N, (void*)&C, (void*)&bh0, (void*)&nblk, (void*)&seed,
                       (void*)&stream_base, (void*)&cent, (void*)&w};
       cudaError_t e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(nh * nblk), dim3(kPPThreads), args, 0, s);
       if (e != cudaSuccess) return e;

@@ -171,16 +171,16 @@ __global__ void k_scatter_rows(const uint4* __restrict__ Op, const int32_t* __re
 
 // FP8 PV path: per (b,h) and channel c the largest |x_c| (bf16 -> f32, as float bits: non-negative floats order like
 // uints).  The grid stride is a multiple of the vectors per row, so a thread always reads the same 8 channels.
-__global__ void k_absmax(const uint4* __restrict__ X, long long vec_per_bh, int vec_per_row,
-                         uint32_t* __restrict__ amax) {
+__global__ void k_absmax(const XView X, long long vec_per_bh, int vec_per_row, uint32_t* __restrict__ amax) {
   const int bh = blockIdx.y;
-  const uint4* Xb = X + size_t(bh) * vec_per_bh;
+  const uint16_t* xb = X.row(bh, 0);
   const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   float m[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) m[e] = 0.f;
   for (long long t = t0; t < vec_per_bh; t += (long long)gridDim.x * blockDim.x) {
-    const uint4 u = __ldg(Xb + t);
+    const long long n = t / vec_per_row;
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(xb + n * X.sN) + (t - n * vec_per_row));
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -203,17 +203,16 @@ __global__ void k_absmax(const uint4* __restrict__ X, long long vec_per_bh, int 
 // FP8 PV path: V' = V[perm] rounded to e4m3, channel c scaled by 448 / amax_c of its head (448 = largest finite e4m3);
 // the attention epilogue multiplies output channel c by amax_c / 448
 __global__ void k_gather_rows_e4m3(const int32_t* __restrict__ perm, long long rows, int N, int vec_per_row,
-                                   const uint4* __restrict__ X, uint2* __restrict__ Xq,
-                                   const uint32_t* __restrict__ amax) {
+                                   const XView X, uint2* __restrict__ Xq, const uint32_t* __restrict__ amax) {
   const long long total = rows * vec_per_row;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const long long r = t / vec_per_row;
     const int v = int(t - r * vec_per_row);
-    const long long bh = r / N;
-    const uint4 u = __ldg(X + (bh * N + __ldg(perm + r)) * vec_per_row + v);
+    const int bh = int(r / N);
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(X.row(bh, __ldg(perm + r))) + v);
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-    const uint32_t* am = amax + (bh * vec_per_row + v) * 8;
+    const uint32_t* am = amax + ((long long)bh * vec_per_row + v) * 8;
     uint32_t q[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -256,7 +255,7 @@ cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, const void* X, void* Xq, uint32_t* amax,
+cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq, uint32_t* amax,
                                     cudaStream_t s) {
   const long long rows = (long long)BH * N;
   const int vpr = d / 8;
@@ -265,9 +264,8 @@ cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int per_bh = (sms * 8 + BH - 1) / BH;
-  k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(static_cast<const uint4*>(X), (long long)N * vpr, vpr, amax);
-  k_gather_rows_e4m3<<<copy_grid(rows * vpr), 256, 0, s>>>(perm, rows, N, vpr, static_cast<const uint4*>(X),
-                                                           static_cast<uint2*>(Xq), amax);
+  k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(X, (long long)N * vpr, vpr, amax);
+  k_gather_rows_e4m3<<<copy_grid(rows * vpr), 256, 0, s>>>(perm, rows, N, vpr, X, static_cast<uint2*>(Xq), amax);
   return cudaGetLastError();
 }
 

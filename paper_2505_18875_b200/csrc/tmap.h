@@ -33,6 +33,21 @@ inline bool make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, int d
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [B, H, N, d] bf16 with element strides (sB, sH, sN), d contiguous: a 4-D map {d, N, H, B}, box 64 columns x box_rows
+// tokens of one head (the same 128-byte-swizzled smem tile as the 2-D map).  Strides must be multiples of 8 elements.
+inline bool make_tmap_bf16_4d(CUtensorMap* m, const void* ptr, int d, int N, int H, int B, long long sN, long long sH,
+                              long long sB, uint32_t box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t gdim[4] = {cuuint64_t(d), cuuint64_t(N), cuuint64_t(H), cuuint64_t(B)};
+  cuuint64_t gstr[3] = {cuuint64_t(sN) * 2, cuuint64_t(sH) * 2, cuuint64_t(sB) * 2};
+  cuuint32_t box[4] = {64, box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), gdim, gstr, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 8-bit elements (e4m3 V' of the FP8 PV path): rows of d bytes, boxes of d bytes x box_rows (one 128-byte swizzle
 // row per token for d = 128)
 inline bool make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t rows, int d, uint32_t box_rows) {
