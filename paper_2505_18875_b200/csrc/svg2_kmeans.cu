@@ -228,7 +228,7 @@ struct SegOut {
   int nch;         // chunks per head at this R
 };
 
-template <int D>
+template <int D, bool kSq>
 __device__ __forceinline__ void store_segment(const SegOut& o, const int32_t* off, int bh, int C, int j, int chunk,
                                               int p0, int p1, int lane, const double* acc, double sq) {
   constexpr int kCols = D / 32;
@@ -237,15 +237,15 @@ __device__ __forceinline__ void store_segment(const SegOut& o, const int32_t* of
   double* dsq;
   if (o0 >= p0 && o1 <= p1) {  // the whole cluster lies in this chunk
     dst = o.sum + (size_t(bh) * C + j) * D;
-    dsq = o.sq ? o.sq + size_t(bh) * C + j : nullptr;
+    dsq = kSq ? o.sq + size_t(bh) * C + j : nullptr;
   } else {
     const size_t slot = (size_t(bh) * o.nch + chunk) * 2 + (o0 <= p0 ? 0 : 1);
     dst = o.part + slot * D;
-    dsq = o.sq ? o.sqpart + slot : nullptr;
+    dsq = kSq ? o.sqpart + slot : nullptr;
   }
 #pragma unroll
   for (int c = 0; c < kCols; ++c) dst[kCols * lane + c] = acc[c];
-  if (dsq) {
+  if (kSq) {
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, s);
     if (lane == 0) *dsq = sq;
@@ -256,7 +256,7 @@ constexpr int kSumRows = 64, kSumUnroll = 8, kSumWarps = 4;
 
 // Plain update (no gather): rows gathered through perm into registers, kSumUnroll loads in flight per warp (lane l
 // holds D/32 consecutive columns, so one row is one coalesced D*2-byte read).
-template <int D>
+template <int D, bool kSq>
 __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, int N, int C,
                                                              const int32_t* __restrict__ perm,
                                                              const int32_t* __restrict__ offsets, SegOut out) {
@@ -267,7 +267,6 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, in
   const int p0 = chunk * kSumRows;
   if (p0 >= N) return;
   const int p1 = min(N, p0 + kSumRows);
-  const bool want_sq = out.sq != nullptr;
   const int32_t* off = offsets + size_t(bh) * (C + 1);
   int lo = 0, hi = C - 1;  // cluster of position p0: last j with off[j] <= p0
   while (lo < hi) {
@@ -282,7 +281,7 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, in
   for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
   bool any = false;
   auto flush = [&] {
-    if (any) store_segment<D>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+    if (any) store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
     for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
     sq = 0.0;
@@ -311,7 +310,7 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, in
         const float2 f = __bfloat1622float2(h[c]);
         acc[2 * c] += double(f.x);
         acc[2 * c + 1] += double(f.y);
-        if (want_sq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
+        if (kSq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
       }
       any = true;
     }
@@ -325,7 +324,7 @@ __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, in
 // tensor (the chunk's rows are contiguous in X').  Measured (ncu, HunyuanVideo): K' + V' 0.69 -> 0.48 ms, Q' equal;
 // for the plain update the register-staged kernel stays faster (0.20 vs 0.33 ms).  Same segmented reduction (R = 32).
 constexpr int kAsyncWarps = 4, kAsyncRows = kUpdMinRows;
-template <int D>
+template <int D, bool kSq>
 __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
     const XView X, int N, int C, const int32_t* __restrict__ perm, const int32_t* __restrict__ offsets, SegOut out,
     __nv_bfloat16* __restrict__ Xp, const XView Y, __nv_bfloat16* __restrict__ Yp) {
@@ -341,7 +340,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   const int p0 = chunk * kRows;
   if (p0 >= N) return;
   const int nrow = min(N - p0, kRows);
-  const bool with_y = Y.p != nullptr, want_sq = out.sq != nullptr;
+  const bool with_y = Y.p != nullptr;
   const int32_t* pm = perm + size_t(bh) * N + p0;
   const int src0 = lane < nrow ? __ldg(pm + lane) : 0;
   const uint8_t* xb = reinterpret_cast<const uint8_t*>(X.row(bh, 0));
@@ -397,7 +396,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   const int p1 = p0 + nrow;
   for (int r = 0; r < nrow; ++r) {
     while (r >= next) {  // crossed into the next cluster: store the segment
-      if (any) store_segment<D>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+      if (any) store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
       sq = 0.0;
@@ -411,11 +410,11 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
       const float2 f = __bfloat1622float2(h[c]);
       acc[2 * c] += double(f.x);
       acc[2 * c + 1] += double(f.y);
-      if (want_sq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
+      if (kSq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
     }
     any = true;
   }
-  if (any) store_segment<D>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+  if (any) store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live
   __syncwarp();
 }
@@ -541,12 +540,14 @@ cudaError_t run_kmeans(const XView X, int BH, int N, int C, int iters, bool warm
     if (gather) {
       const dim3 grid_a((N + kAsyncRows * kAsyncWarps - 1) / (kAsyncRows * kAsyncWarps), BH);
       const size_t sm = size_t(kAsyncWarps) * 2 * kAsyncRows * D * 2;
-      cudaFuncSetAttribute(k_update_sum_async<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-      k_update_sum_async<D><<<grid_a, 32 * kAsyncWarps, sm, s>>>(
-          X, N, C, perm, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp), g.Y, static_cast<__nv_bfloat16*>(g.Yp));
+      auto kern = objective ? k_update_sum_async<D, true> : k_update_sum_async<D, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+      kern<<<grid_a, 32 * kAsyncWarps, sm, s>>>(X, N, C, perm, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp), g.Y,
+                                                static_cast<__nv_bfloat16*>(g.Yp));
     } else {
       const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
-      k_update_sum<D><<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, seg);
+      auto kern = objective ? k_update_sum<D, true> : k_update_sum<D, false>;
+      kern<<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, seg);
     }
     k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, R, offsets, seg, cent, objective ? ws.j_part : nullptr);
     if (objective) k_objective<<<(BH + 127) / 128, 128, 0, s>>>(BH, C, ws.j_part, objective + size_t(it) * BH * 2);

@@ -16,6 +16,6 @@ for spec in "$@"; do
   name=${spec%%:*}
   for r in $(seq 1 "$reps"); do
     echo -n "${name}_${r} "
-    tail -1 "gpurun_out/ab_${name}_${r}.log" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],2), round(d['stages_ms']['attention'],2), d['clocks']['sm_mhz'], round(d['roofline']['frac'],3), round(d['density'],4))" 2>&1 | tail -1
+    tail -1 "gpurun_out/ab_${name}_${r}.log" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],2), round(d['stages_ms']['attention'],2), d['clocks']['sm_mhz'], round(d['roofline']['frac'],3), round(d['density'],4), 'kmeans', round(d['stages_ms']['kmeans_k']+d['stages_ms']['kmeans_q'],3))" 2>&1 | tail -1
   done
 done
