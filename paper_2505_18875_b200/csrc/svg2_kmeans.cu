@@ -252,106 +252,109 @@ __device__ __forceinline__ void store_segment(const SegOut& o, const int32_t* of
   }
 }
 
-constexpr int kSumRows = 64, kSumUnroll = 8, kSumWarps = 4;
+constexpr int kSumRows = 64, kSumUnroll = 16, kSumWarps = 4;
 
 // Plain update (no gather): rows gathered through perm into registers, kSumUnroll loads in flight per warp (lane l
-// holds D/32 consecutive columns, so one row is one coalesced D*2-byte read).
+// holds D/32 consecutive columns, so one row is one coalesced D*2-byte read).  The chunk's perm entries and their
+// labels (two per lane) are loaded up front; a segment ends where the label changes.
 template <int D, bool kSq>
 __global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, int N, int C,
                                                              const int32_t* __restrict__ perm,
+                                                             const int32_t* __restrict__ labels,
                                                              const int32_t* __restrict__ offsets, SegOut out) {
   constexpr int kCols = D / 32;  // 4 (d = 128) or 2 (d = 64) bf16 per lane
   using Vec = typename std::conditional<kCols == 4, uint2, uint32_t>::type;
+  static_assert(kSumRows == 64, "two perm entries per lane");
   const int bh = blockIdx.y, lane = threadIdx.x & 31;
   const int chunk = blockIdx.x * kSumWarps + (threadIdx.x >> 5);
   const int p0 = chunk * kSumRows;
   if (p0 >= N) return;
-  const int p1 = min(N, p0 + kSumRows);
+  const int p1 = min(N, p0 + kSumRows), nrow = p1 - p0;
   const int32_t* off = offsets + size_t(bh) * (C + 1);
-  int lo = 0, hi = C - 1;  // cluster of position p0: last j with off[j] <= p0
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(off + mid) <= p0) lo = mid; else hi = mid - 1;
-  }
-  int j = lo, next = __ldg(off + j + 1);
+  const int32_t* pm = perm + size_t(bh) * N + p0;
+  const int32_t* lb = labels + size_t(bh) * N;
+  const int s0 = lane < nrow ? __ldg(pm + lane) : 0, s1 = lane + 32 < nrow ? __ldg(pm + 32 + lane) : 0;
+  const int l0 = lane < nrow ? __ldg(lb + s0) : 0, l1 = lane + 32 < nrow ? __ldg(lb + s1) : 0;
   const uint16_t* xb = X.row(bh, 0);
-  const int32_t* pm = perm + size_t(bh) * N;
+  int j = __shfl_sync(0xffffffffu, l0, 0);
   double acc[kCols], sq = 0.0;
 #pragma unroll
   for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-  bool any = false;
-  auto flush = [&] {
-    if (any) store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
-    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-    sq = 0.0;
-    any = false;
-  };
-  for (int pb = p0; pb < p1; pb += kSumUnroll) {
-    const int src_l = pb + (lane & (kSumUnroll - 1)) < p1 ? __ldg(pm + pb + (lane & (kSumUnroll - 1))) : 0;
-    Vec v[kSumUnroll];
+  for (int half = 0; half < 2; ++half) {
+    const int sh = half ? s1 : s0, lh = half ? l1 : l0;
 #pragma unroll
-    for (int u = 0; u < kSumUnroll; ++u) {
-      const int src = __shfl_sync(0xffffffffu, src_l, u);
-      if (pb + u < p1) v[u] = __ldg(reinterpret_cast<const Vec*>(xb + src * X.sN) + lane);
-    }
+    for (int pb = 0; pb < 32; pb += kSumUnroll) {
+      const int base = 32 * half + pb;
+      if (base >= nrow) break;
+      Vec v[kSumUnroll];
 #pragma unroll
-    for (int u = 0; u < kSumUnroll; ++u) {
-      const int pos = pb + u;
-      if (pos >= p1) break;
-      while (pos >= next) {  // crossed into the next cluster: store the segment
-        flush();
-        ++j;
-        next = __ldg(off + j + 1);
+      for (int u = 0; u < kSumUnroll; ++u) {
+        const int src = __shfl_sync(0xffffffffu, sh, pb + u);
+        if (base + u < nrow) v[u] = __ldg(reinterpret_cast<const Vec*>(xb + src * X.sN) + lane);
       }
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
 #pragma unroll
-      for (int c = 0; c < kCols / 2; ++c) {
-        const float2 f = __bfloat1622float2(h[c]);
-        acc[2 * c] += double(f.x);
-        acc[2 * c + 1] += double(f.y);
-        if (kSq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
+      for (int u = 0; u < kSumUnroll; ++u) {
+        const int lab = __shfl_sync(0xffffffffu, lh, pb + u);
+        if (base + u >= nrow) break;
+        if (lab != j) {  // the next cluster starts: store the segment
+          store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+          sq = 0.0;
+          j = lab;
+        }
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+        for (int c = 0; c < kCols / 2; ++c) {
+          const float2 f = __bfloat1622float2(h[c]);
+          acc[2 * c] += double(f.x);
+          acc[2 * c + 1] += double(f.y);
+          if (kSq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
+        }
       }
-      any = true;
     }
   }
-  flush();
+  store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 }
 
 // The last (gather) iteration's pass with the row gathers as asynchronous copies (cp.async, 16 B per
-// lane-instruction): a warp puts all kAsyncRows rows of its chunk (X and Y) in flight at once through shared memory
+// lane-instruction): a warp puts all kRows rows of its chunk (X and Y) in flight at once through shared memory
 // instead of kSumUnroll rows through registers, and the permuted copies leave shared memory as one bulk copy per
-// tensor (the chunk's rows are contiguous in X').  Measured (ncu, HunyuanVideo): K' + V' 0.69 -> 0.48 ms, Q' equal;
-// for the plain update the register-staged kernel stays faster (0.20 vs 0.33 ms).  Same segmented reduction (R = 32).
-constexpr int kAsyncWarps = 4, kAsyncRows = kUpdMinRows;
-template <int D, bool kSq>
+// tensor (the chunk's rows are contiguous in X').  kRows = 32 with a second tensor (K and V), 64 for X alone (Q):
+// the same 16 KB of shared memory per warp.  Same segmented reduction (R = kRows), segments cut at label changes.
+constexpr int kAsyncWarps = 4, kAsyncRowBytes = 2 * kUpdMinRows * 256;  // per warp: 16 KB (d = 128)
+template <int D, bool kSq, int kRows>
 __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
-    const XView X, int N, int C, const int32_t* __restrict__ perm, const int32_t* __restrict__ offsets, SegOut out,
-    __nv_bfloat16* __restrict__ Xp, const XView Y, __nv_bfloat16* __restrict__ Yp) {
+    const XView X, int N, int C, const int32_t* __restrict__ perm, const int32_t* __restrict__ labels,
+    const int32_t* __restrict__ offsets, SegOut out, __nv_bfloat16* __restrict__ Xp, const XView Y,
+    __nv_bfloat16* __restrict__ Yp) {
   constexpr int kCols = D / 32;           // bf16 per lane in the accumulation
   constexpr int kRowBytes = D * 2;        // 256 (d = 128) or 128 (d = 64)
   constexpr int kVecPerRow = kRowBytes / 16;
-  constexpr int kRows = kAsyncRows;
+  static_assert(kRows == 32 || kRows == 64, "one or two perm entries per lane");
   extern __shared__ __align__(128) uint8_t sm_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, bh = blockIdx.y;
-  uint8_t* sx = sm_raw + size_t(warp) * 2 * kRows * kRowBytes;  // [kRows][row] X rows of this warp
-  uint8_t* sy = sx + kRows * kRowBytes;                          // [kRows][row] Y rows
+  uint8_t* sx = sm_raw + size_t(warp) * kAsyncRowBytes;  // [kRows][row] X rows of this warp
+  uint8_t* sy = sx + kRows * kRowBytes;                  // [kRows][row] Y rows (kRows = 32)
   const int chunk = blockIdx.x * kAsyncWarps + warp;
   const int p0 = chunk * kRows;
   if (p0 >= N) return;
   const int nrow = min(N - p0, kRows);
   const bool with_y = Y.p != nullptr;
   const int32_t* pm = perm + size_t(bh) * N + p0;
-  const int src0 = lane < nrow ? __ldg(pm + lane) : 0;
+  const int s0 = lane < nrow ? __ldg(pm + lane) : 0;
+  const int s1 = kRows > 32 && lane + 32 < nrow ? __ldg(pm + 32 + lane) : 0;
   const uint8_t* xb = reinterpret_cast<const uint8_t*>(X.row(bh, 0));
   const uint8_t* yb = with_y ? reinterpret_cast<const uint8_t*>(Y.row(bh, 0)) : nullptr;
   const long long xrow = X.sN * 2, yrow = Y.sN * 2;  // bytes between tokens
   // issue: 32 lanes cover 32 / kVecPerRow rows per step, one 16-byte piece each
   constexpr int kRowsPerStep = 32 / kVecPerRow;
   const int piece = lane % kVecPerRow, rsub = lane / kVecPerRow;
-  for (int r0 = 0; r0 < nrow; r0 += kRowsPerStep) {
+#pragma unroll 4
+  for (int r0 = 0; r0 < kRows; r0 += kRowsPerStep) {
     const int r = r0 + rsub;
-    const int src = __shfl_sync(0xffffffffu, src0, r & 31);
+    const int src = __shfl_sync(0xffffffffu, r < 32 ? s0 : s1, r & 31);
     if (r < nrow) {
       const uint32_t dst = smem_u32(sx + r * kRowBytes + piece * 16);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(xb + src * xrow + piece * 16)
@@ -363,14 +366,11 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
       }
     }
   }
-  // cluster of the first position while the copies fly: last j with off[j] <= p0
+  // the rows' labels while the copies fly
+  const int32_t* lb = labels + size_t(bh) * N;
+  const int l0 = lane < nrow ? __ldg(lb + s0) : 0;
+  const int l1 = kRows > 32 && lane + 32 < nrow ? __ldg(lb + s1) : 0;
   const int32_t* off = offsets + size_t(bh) * (C + 1);
-  int lo = 0, hi = C - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(off + mid) <= p0) lo = mid; else hi = mid - 1;
-  }
-  int j = lo, next = __ldg(off + j + 1) - p0;  // positions relative to p0
   asm volatile("cp.async.wait_all;" ::: "memory");
   // every lane's cp.async writes into shared memory are made visible to the async proxy (the bulk store below) by
   // that lane's own proxy fence before the warp barrier
@@ -392,17 +392,16 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   double acc[kCols], sq = 0.0;
 #pragma unroll
   for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-  bool any = false;
   const int p1 = p0 + nrow;
+  int j = __shfl_sync(0xffffffffu, l0, 0);
   for (int r = 0; r < nrow; ++r) {
-    while (r >= next) {  // crossed into the next cluster: store the segment
-      if (any) store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+    const int lab = __shfl_sync(0xffffffffu, r < 32 ? l0 : l1, r & 31);
+    if (lab != j) {  // the next cluster starts: store the segment
+      store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
       for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
       sq = 0.0;
-      any = false;
-      ++j;
-      next = __ldg(off + j + 1) - p0;
+      j = lab;
     }
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(sx + r * kRowBytes + lane * kCols * 2);
 #pragma unroll
@@ -412,9 +411,8 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
       acc[2 * c + 1] += double(f.y);
       if (kSq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
     }
-    any = true;
   }
-  if (any) store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
+  store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live
   __syncwarp();
 }
@@ -535,19 +533,20 @@ cudaError_t run_kmeans(const XView X, int BH, int N, int C, int iters, bool warm
     // plain update keeps the register-staged one (0.20 ms vs 0.33 ms: its accumulation phase has no loads in flight)
     if (it + 1 == iters && g.wait_y) cudaStreamWaitEvent(s, g.wait_y, 0);
     const bool gather = it + 1 == iters && g.Xp;
-    const int R = gather ? kAsyncRows : kSumRows;
+    const int R = gather ? (g.Y.p ? 32 : 64) : kSumRows;
     SegOut seg{ws.c_sum, ws.c_part, objective ? ws.c_sq : nullptr, ws.c_sqpart, (N + R - 1) / R};
     if (gather) {
-      const dim3 grid_a((N + kAsyncRows * kAsyncWarps - 1) / (kAsyncRows * kAsyncWarps), BH);
-      const size_t sm = size_t(kAsyncWarps) * 2 * kAsyncRows * D * 2;
-      auto kern = objective ? k_update_sum_async<D, true> : k_update_sum_async<D, false>;
+      const dim3 grid_a((N + R * kAsyncWarps - 1) / (R * kAsyncWarps), BH);
+      const size_t sm = size_t(kAsyncWarps) * kAsyncRowBytes;
+      auto kern = g.Y.p ? (objective ? k_update_sum_async<D, true, 32> : k_update_sum_async<D, false, 32>)
+                        : (objective ? k_update_sum_async<D, true, 64> : k_update_sum_async<D, false, 64>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-      kern<<<grid_a, 32 * kAsyncWarps, sm, s>>>(X, N, C, perm, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp), g.Y,
-                                                static_cast<__nv_bfloat16*>(g.Yp));
+      kern<<<grid_a, 32 * kAsyncWarps, sm, s>>>(X, N, C, perm, labels, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp),
+                                                g.Y, static_cast<__nv_bfloat16*>(g.Yp));
     } else {
       const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
       auto kern = objective ? k_update_sum<D, true> : k_update_sum<D, false>;
-      kern<<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, offsets, seg);
+      kern<<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, labels, offsets, seg);
     }
     k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, R, offsets, seg, cent, objective ? ws.j_part : nullptr);
     if (objective) k_objective<<<(BH + 127) / 128, 128, 0, s>>>(BH, C, ws.j_part, objective + size_t(it) * BH * 2);

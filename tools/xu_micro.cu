@@ -29,6 +29,22 @@ __device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
   return y;
 }
 
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  uint32_t r;
+  asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 template <int kMode>
 __global__ void k_bench(float* out, long long* cyc, float seed) {
   float v[kChains];
@@ -49,6 +65,18 @@ __global__ void k_bench(float* out, long long* cyc, float seed) {
         uint32_t u = __float_as_uint(v[c]);
         u = ex2_bf16x2(u & 0xBFFFBFFFu);
         v[c] = __uint_as_float(u & 0x3F7F3F7Fu);
+      }
+      if (kMode == 9) {  // packed f16x2 exp2 on a dependent chain (2 results per op?)
+        uint32_t u = __float_as_uint(v[c]);
+        u = ex2_f16x2(u & 0xBBFFBBFFu);
+        v[c] = __uint_as_float(u & 0x3BFF3BFFu);
+      }
+      if (kMode == 10) acc += pack_f16(v[c], v[(c + 1) % kChains]), v[c] += 1e-7f * float(acc & 1u);  // F2FP.F16
+      if (kMode == 11) {  // the f16 softmax shape: x = s*c - m (FFMA2), cvt to f16x2, ex2.f16x2, HADD2 row sum
+        const float x0 = fmaf(v[c], 1.4427f, -float(i & 7)), x1 = fmaf(v[(c + 1) % kChains], 1.4427f, -float(i & 3));
+        const uint32_t p = ex2_f16x2(pack_f16(x0, x1));
+        acc = hadd2(acc, p);
+        v[c] += 1e-9f * float(p & 1u);
       }
       if (kMode >= 5 && kMode <= 7) {  // independent inputs: the real softmax shape (x = s*c - m; p = ex2(x); sum; pack)
         const float x0 = fmaf(v[c], 1.4427f, -float(i & 7)), x1 = fmaf(v[(c + 1) % kChains], 1.4427f, -float(i & 3));
@@ -100,5 +128,8 @@ int main() {
   run<6>("indep: + F2FP", 2 * kChains, kChains);
   run<7>("indep: + ALU pack", 2 * kChains, kChains);
   run<8>("ex2.bf16x2 (2 per op)", 2 * kChains, 0);
+  run<9>("ex2.f16x2 (2 per op)", 2 * kChains, 0);
+  run<10>("F2FP.F16 pack only", 0, kChains);
+  run<11>("indep f16: ffma cvt ex2x2 hadd2", 2 * kChains, kChains);
   return 0;
 }
