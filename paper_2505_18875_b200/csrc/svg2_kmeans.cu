@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t cc = 0;
+      int held[2] = {-1, -1};  // head whose (single) centroid chunk a stage holds
       for (int u = u0, i = 0; u < u1; ++u, ++i) {
         const int bh = u / upb, row0 = (u - bh * upb) * kAsgRows;
         const int xs = i & 1;
@@ -122,6 +123,11 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         for (int c = 0; c < nchunks; ++c, ++cc) {
           const int s = cc & 1;
           mbar_wait(&bars.c_empty[s], ((cc >> 1) & 1) ^ 1);
+          if (nchunks == 1 && held[s] == bh) {  // C <= 128: the stage still holds this head's centroids
+            mbar_arrive(&bars.c_full[s]);
+            continue;
+          }
+          if (nchunks == 1) held[s] = bh;
           mbar_arrive_expect_tx(&bars.c_full[s], 2 * C::kTileBytes);
           const int crow = bh * Cpad + c * kCentChunk;
           for (int b = 0; b < C::kBlocks; ++b) {

@@ -53,22 +53,24 @@ def accuracy(O, ref):
             "psnr_db": 10 * math.log10(peak * peak / mse) if mse > 0 else float("inf")}
 
 
-def run_point(Q, K, V, ref, wl, Cq, Ck, p, reps=3):
+def run_point(Q, K, V, ref, wl, Cq, Ck, p, reps=5):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
     O, pairs, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, wl.iters, p)
     cq, ck = ex["q_centroids"], ex["k_centroids"]
     svg2.sparse_attention(Q, K, V, Cq, Ck, 2, p, cq, ck, warm=True)
     torch.cuda.synchronize()
-    t_call = t_attn = 0.0
     names = ["kmeans_k_fork", "kmeans_q_join", "permute_fp8", "select_topp", "worklist", "attention", "end"]
-    stages = {n: 0.0 for n in names}
-    for _ in range(reps):
+    calls, attns, per_stage = [], [], {n: [] for n in names}
+    for _ in range(reps):  # medians over the repetitions (a host stall in one call does not move the result)
         O, pairs, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, 2, p, cq, ck, warm=True, events=ev, debug=True)
         torch.cuda.synchronize()
-        t_call += ev[0].elapsed_time(ev[7]) / reps
-        t_attn += ev[5].elapsed_time(ev[6]) / reps
+        calls.append(ev[0].elapsed_time(ev[7]))
+        attns.append(ev[5].elapsed_time(ev[6]))
         for i, n in enumerate(names):
-            stages[n] += ev[i].elapsed_time(ev[i + 1]) / reps
+            per_stage[n].append(ev[i].elapsed_time(ev[i + 1]))
+    med = lambda a: sorted(a)[len(a) // 2]  # noqa: E731
+    t_call, t_attn = med(calls), med(attns)
+    stages = {n: med(v) for n, v in per_stage.items()}
     B, H, N, d = Q.shape
     dens = float(pairs.double().sum()) / (B * H * N * N)
     alg, exe, static = tile_work(ex["q_offsets"], ex["k_offsets"], ex["mask"])
@@ -92,14 +94,17 @@ def main():
     del q, k, v
     from torch.nn.attention import SDPBackend, sdpa_kernel
     with sdpa_kernel([SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION]):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ref = torch.nn.functional.scaled_dot_product_attention(Q, K, V)
-        torch.cuda.synchronize()
-        s.record()
-        ref = torch.nn.functional.scaled_dot_product_attention(Q, K, V)
-        e.record()
-        torch.cuda.synchronize()
-        t_dense = s.elapsed_time(e)
+        times = []
+        for _ in range(5):  # median of 5 timed calls
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s.record()
+            ref = torch.nn.functional.scaled_dot_product_attention(Q, K, V)
+            e.record()
+            torch.cuda.synchronize()
+            times.append(s.elapsed_time(e))
+        t_dense = sorted(times)[2]
     res = {"workload": wl.name, "heads": args.heads, "N": wl.N, "dense_ms_sdpa": t_dense, "topp_sweep": [],
            "cluster_sweep": []}
     if args.points:
