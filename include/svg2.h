@@ -172,9 +172,9 @@ SVG2_API svg2_status_t svg2_unpermute(const void* Op, const int32_t* perm, int32
  * attention with the unpermute fused into its epilogue.  O [B,H,Nq,d] bf16 out in original token order.
  * selected_pairs [B,H] int64 out (nullable).  dbg: NULL or intermediates / stage events (see svg2_debug_t).
  * Streams: the K-role k-means runs on a (high-priority) stream forked from `stream` for the duration of the call
- * (event fork /
- * join, created and released per call; not while `stream` is being captured into a CUDA graph, where the call
- * stays on `stream` and is capture-safe); all work is ordered after, and joined back into, `stream`. */
+ * (event fork / join; the stream and events are created and released per call unless the caller lends them through
+ * svg2_layout_t.aux_*; without lent ones the call stays on `stream` while `stream` is being captured into a CUDA
+ * graph); all work is ordered after, and joined back into, `stream`. */
 SVG2_API svg2_status_t svg2_sparse_attention(const void* Q, const void* K, const void* V, svg2_dims_t dims,
                                     const svg2_config_t* config, float* q_centroids, float* k_centroids, void* O,
                                     int64_t* selected_pairs, const svg2_debug_t* dbg, void* ws, size_t ws_bytes,
@@ -206,13 +206,17 @@ SVG2_API svg2_status_t svg2_sparse_attention_ex(const void* Q, const void* K, co
  *                  the query clusters of parts [part_begin, part_end) of part_count -- per head, cluster i with cost
  *                  c_i = |Q_i| * keys_i (its selected pairs) and preceding cost P_i belongs to part
  *                  floor((2 P_i + c_i) part_count / (2 T)), T the head's total -- and writes only their rows.
- *                  {0, 0, 0} = all clusters.  selected_pairs and the centroid caches are always the whole head's. */
+ *                  {0, 0, 0} = all clusters.  selected_pairs and the centroid caches are always the whole head's.
+ *   aux_stream / aux_events  optional resources for the forked K-role stream (see svg2_sparse_attention). */
 typedef struct {
   int64_t q_strides[3], k_strides[3], v_strides[3];
   void* const* o_shards;
   int32_t n_shards, shard_tokens, o_head_offset, part_begin;
   int64_t o_strides[3];
   int32_t part_end, part_count;
+  void* aux_stream;     /* NULL, or a caller-owned cudaStream_t (high priority recommended) for the K-role k-means */
+  void* aux_events[2];  /* with aux_stream: two caller-owned cudaEvent_t (fork, join); then the call creates no stream
+                           or event of its own, and the role overlap also works inside CUDA graph capture */
 } svg2_layout_t;
 
 /* The fused call with a layout (NULL layout == svg2_sparse_attention_ex). */

@@ -61,10 +61,28 @@ class Layout(ctypes.Structure):
     _fields_ = [("q_strides", ctypes.c_int64 * 3), ("k_strides", ctypes.c_int64 * 3), ("v_strides", ctypes.c_int64 * 3),
                 ("o_shards", ctypes.c_void_p), ("n_shards", ctypes.c_int32), ("shard_tokens", ctypes.c_int32),
                 ("o_head_offset", ctypes.c_int32), ("part_begin", ctypes.c_int32), ("o_strides", ctypes.c_int64 * 3),
-                ("part_end", ctypes.c_int32), ("part_count", ctypes.c_int32)]
+                ("part_end", ctypes.c_int32), ("part_count", ctypes.c_int32), ("aux_stream", ctypes.c_void_p),
+                ("aux_events", ctypes.c_void_p * 2)]
 
 
 _lib = None
+_aux_cache: dict = {}
+
+
+def _aux(device):
+    """A high-priority stream and two events per device, lent to the fused call for its K-role fork (created once, so
+    the call creates no CUDA objects of its own and keeps the role overlap under CUDA graph capture)."""
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    got = _aux_cache.get(key)
+    if got is None:
+        with torch.cuda.device(key):
+            st = torch.cuda.Stream(priority=-1)
+            evs = [torch.cuda.Event(enable_timing=False) for _ in range(2)]
+            for ev in evs:
+                ev.record(st)  # materialise the handle
+        got = (st, evs)
+        _aux_cache[key] = got
+    return got
 
 
 def load_library(path: str = LIB_PATH):
@@ -316,6 +334,9 @@ def sparse_attention(Q, K, V, Cq: int, Ck: int, iters: int, top_p: float, q_cent
     dims = Dims(B, H, Nq, Nk, d)
     lay = Layout()
     keep = []
+    st, evs = _aux(dev)
+    lay.aux_stream = st.cuda_stream
+    lay.aux_events[0], lay.aux_events[1] = evs[0].cuda_event, evs[1].cuda_event
     for t, name in ((Q, "q_strides"), (K, "k_strides"), (V, "v_strides")):
         if not t.is_contiguous():
             st = [t.stride(0), t.stride(1), t.stride(2)]

@@ -50,6 +50,11 @@ svg2_status_t pending_error() { return from_cuda(cudaGetLastError()); }
 
 float resolve_scale(float scale, int d) { return scale > 0.f ? scale : float(1.0 / std::sqrt(double(d))); }
 
+struct AuxStream {  // a caller-owned stream and two events for the K-role fork (svg2_layout_t.aux_*)
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
 struct FusedWs {
   int32_t *lab_q, *lab_k, *perm_q, *perm_k, *off_q, *off_k, *size_q, *size_k;
   void *Qp, *Kp, *Vp;
@@ -104,7 +109,7 @@ svg2_status_t validate_fused(const svg2_dims_t& dm, const svg2_config_t* cfg) {
 cudaError_t run_fused(const XView& Q, const XView& K, const XView& V, const svg2_dims_t& dm, const svg2_config_t* cfg,
                       float* q_centroids, float* k_centroids, const OutView& out, int64_t* selected_pairs,
                       const svg2_debug_t* dbg, FusedWs w, cudaStream_t s, int bh_base,
-                      const cudaEvent_t* arrive = nullptr, QPart part = QPart()) {
+                      const cudaEvent_t* arrive = nullptr, QPart part = QPart(), const AuxStream* aux = nullptr) {
   // arrive (host pipeline): events of Q, K and V landing in device memory; each role waits only for its own tensor,
   // V only before the pass that gathers it
   if (dbg) {  // intermediates requested: write them straight into the caller's buffers
@@ -150,9 +155,19 @@ cudaError_t run_fused(const XView& Q, const XView& K, const XView& V, const svg2
   // launches) stays on one stream.
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  const bool pp_cold = !warm && init_q.kmeanspp;
+  const bool own = !(aux && aux->stream);  // the caller may lend a stream and two events (no per-call creation)
   cudaStreamCaptureStatus capture = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &capture);  // inside a graph capture: stay on the caller's stream (no stream creation)
-  if (!(!warm && init_q.kmeanspp) && capture == cudaStreamCaptureStatusNone) {
+  cudaStreamIsCapturing(s, &capture);  // capturing: only a lent stream forks (event fork / join is capture-legal)
+  if (!pp_cold && !own) {
+    s2 = aux->stream;
+    ev_fork = aux->fork;
+    ev_join = aux->join;
+    if (cudaEventRecord(ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(s2, ev_fork, 0) != cudaSuccess) {
+      s2 = nullptr;
+      (void)cudaGetLastError();
+    }
+  } else if (!pp_cold && capture == cudaStreamCaptureStatusNone) {
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
     if (cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio_high) !=
@@ -180,10 +195,10 @@ cudaError_t run_fused(const XView& Q, const XView& K, const XView& V, const svg2
   if (s2) {  // join (always, so no work is left behind on s2 even after an error) and release (deferred by CUDA)
     cudaEventRecord(ev_join, s2);
     cudaStreamWaitEvent(s, ev_join, 0);
-    cudaStreamDestroy(s2);
+    if (own) cudaStreamDestroy(s2);
   }
-  if (ev_fork) cudaEventDestroy(ev_fork);
-  if (ev_join) cudaEventDestroy(ev_join);
+  if (own && ev_fork) cudaEventDestroy(ev_fork);
+  if (own && ev_join) cudaEventDestroy(ev_join);
   mark(2);
   if (arrive && !gk.wait_y) cudaStreamWaitEvent(s, arrive[2], 0);  // V gathered by a separate pass (FP8 PV)
   // FP8 PV (R26): V' in e4m3 with a per-head scale, written into the first half of the bf16 V' buffer
@@ -495,6 +510,13 @@ svg2_status_t svg2_sparse_attention_layout(const void* Q, const void* K, const v
     return SVG2_ERR_MISALIGNED;
   QPart part;
   OutView out = contiguous_out(O, dm.H, dm.Nq, dm.d);
+  AuxStream aux;
+  if (lay && lay->aux_stream) {
+    if (!lay->aux_events[0] || !lay->aux_events[1]) return SVG2_ERR_NULL_POINTER;
+    aux.stream = static_cast<cudaStream_t>(lay->aux_stream);
+    aux.fork = static_cast<cudaEvent_t>(lay->aux_events[0]);
+    aux.join = static_cast<cudaEvent_t>(lay->aux_events[1]);
+  }
   if (lay) {
     const int64_t* strs[3] = {lay->q_strides, lay->k_strides, lay->v_strides};
     for (int t = 0; t < 3; ++t)
@@ -537,7 +559,7 @@ svg2_status_t svg2_sparse_attention_layout(const void* Q, const void* K, const v
   const XView kv = view_of(K, dm, dm.Nk, lay ? lay->k_strides : nullptr);
   const XView vv = view_of(V, dm, dm.Nk, lay ? lay->v_strides : nullptr);
   return from_cuda(run_fused(qv, kv, vv, dm, cfg, q_centroids, k_centroids, out, selected_pairs, dbg, w,
-                             static_cast<cudaStream_t>(stream), 0, input_ready ? ready : nullptr, part));
+                             static_cast<cudaStream_t>(stream), 0, input_ready ? ready : nullptr, part, &aux));
 }
 
 svg2_status_t svg2_sparse_attention_host(const void* Qh, const void* Kh, const void* Vh, svg2_dims_t dm,
