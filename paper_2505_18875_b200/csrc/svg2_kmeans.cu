@@ -258,77 +258,12 @@ __device__ __forceinline__ void store_segment(const SegOut& o, const int32_t* of
   }
 }
 
-constexpr int kSumRows = 64, kSumUnroll = 16, kSumWarps = 4;
-
-// Plain update (no gather): rows gathered through perm into registers, kSumUnroll loads in flight per warp (lane l
-// holds D/32 consecutive columns, so one row is one coalesced D*2-byte read).  The chunk's perm entries and their
-// labels (two per lane) are loaded up front; a segment ends where the label changes.
-template <int D, bool kSq>
-__global__ void __launch_bounds__(32 * kSumWarps) k_update_sum(const XView X, int N, int C,
-                                                             const int32_t* __restrict__ perm,
-                                                             const int32_t* __restrict__ labels,
-                                                             const int32_t* __restrict__ offsets, SegOut out) {
-  constexpr int kCols = D / 32;  // 4 (d = 128) or 2 (d = 64) bf16 per lane
-  using Vec = typename std::conditional<kCols == 4, uint2, uint32_t>::type;
-  static_assert(kSumRows == 64, "two perm entries per lane");
-  const int bh = blockIdx.y, lane = threadIdx.x & 31;
-  const int chunk = blockIdx.x * kSumWarps + (threadIdx.x >> 5);
-  const int p0 = chunk * kSumRows;
-  if (p0 >= N) return;
-  const int p1 = min(N, p0 + kSumRows), nrow = p1 - p0;
-  const int32_t* off = offsets + size_t(bh) * (C + 1);
-  const int32_t* pm = perm + size_t(bh) * N + p0;
-  const int32_t* lb = labels + size_t(bh) * N;
-  const int s0 = lane < nrow ? __ldg(pm + lane) : 0, s1 = lane + 32 < nrow ? __ldg(pm + 32 + lane) : 0;
-  const int l0 = lane < nrow ? __ldg(lb + s0) : 0, l1 = lane + 32 < nrow ? __ldg(lb + s1) : 0;
-  const uint16_t* xb = X.row(bh, 0);
-  int j = __shfl_sync(0xffffffffu, l0, 0);
-  double acc[kCols], sq = 0.0;
-#pragma unroll
-  for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int sh = half ? s1 : s0, lh = half ? l1 : l0;
-#pragma unroll
-    for (int pb = 0; pb < 32; pb += kSumUnroll) {
-      const int base = 32 * half + pb;
-      if (base >= nrow) break;
-      Vec v[kSumUnroll];
-#pragma unroll
-      for (int u = 0; u < kSumUnroll; ++u) {
-        const int src = __shfl_sync(0xffffffffu, sh, pb + u);
-        if (base + u < nrow) v[u] = __ldg(reinterpret_cast<const Vec*>(xb + src * X.sN) + lane);
-      }
-#pragma unroll
-      for (int u = 0; u < kSumUnroll; ++u) {
-        const int lab = __shfl_sync(0xffffffffu, lh, pb + u);
-        if (base + u >= nrow) break;
-        if (lab != j) {  // the next cluster starts: store the segment
-          store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
-#pragma unroll
-          for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-          sq = 0.0;
-          j = lab;
-        }
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
-#pragma unroll
-        for (int c = 0; c < kCols / 2; ++c) {
-          const float2 f = __bfloat1622float2(h[c]);
-          acc[2 * c] += double(f.x);
-          acc[2 * c + 1] += double(f.y);
-          if (kSq) sq += double(f.x) * double(f.x) + double(f.y) * double(f.y);
-        }
-      }
-    }
-  }
-  store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
-}
-
-// The last (gather) iteration's pass with the row gathers as asynchronous copies (cp.async, 16 B per
-// lane-instruction): a warp puts all kRows rows of its chunk (X and Y) in flight at once through shared memory
-// instead of kSumUnroll rows through registers, and the permuted copies leave shared memory as one bulk copy per
-// tensor (the chunk's rows are contiguous in X').  kRows = 32 with a second tensor (K and V), 64 for X alone (Q):
-// the same 16 KB of shared memory per warp.  Same segmented reduction (R = kRows), segments cut at label changes.
+// The update pass: row gathers through perm as asynchronous copies (cp.async, 16 B per lane-instruction), a warp puts
+// all kRows rows of its chunk in flight at once through shared memory (kRows = 64, or 32 rows each of X and Y when
+// the last pass also gathers V through the same pi_k: 16 KB per warp either way); the chunk's perm entries and their
+// labels are loaded up front and a segment ends where the label changes.  On the last Lloyd iteration of the fused
+// call (Xp set) the permuted copies leave shared memory as one bulk copy per tensor (the chunk's rows are contiguous
+// in X', A6).
 constexpr int kAsyncWarps = 4, kAsyncRowBytes = 2 * kUpdMinRows * 256;  // per warp: 16 KB (d = 128)
 template <int D, bool kSq, int kRows>
 __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
@@ -382,7 +317,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   // that lane's own proxy fence before the warp barrier
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
-  if (lane == 0) {  // X' (and Y') rows p0 .. p0 + nrow - 1 are contiguous: one bulk store each
+  if (Xp != nullptr && lane == 0) {  // X' (and Y') rows p0 .. p0 + nrow - 1 are contiguous: one bulk store each
     uint8_t* gx = reinterpret_cast<uint8_t*>(Xp) + (size_t(bh) * N + p0) * kRowBytes;
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gx), "r"(smem_u32(sx)),
                  "r"(nrow * kRowBytes)
@@ -419,7 +354,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
     }
   }
   store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live
+  if (Xp != nullptr && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live
   __syncwarp();
 }
 
@@ -538,22 +473,21 @@ cudaError_t run_kmeans(const XView X, int BH, int N, int C, int iters, bool warm
     // the gather pass (last iteration) uses the asynchronous-copy kernel: K' + V' 0.69 -> 0.48 ms, Q' equal; the
     // plain update keeps the register-staged one (0.20 ms vs 0.33 ms: its accumulation phase has no loads in flight)
     if (it + 1 == iters && g.wait_y) cudaStreamWaitEvent(s, g.wait_y, 0);
+    // every update pass: the rows of a warp's chunk arrive by cp.async through shared memory (64 rows, or 32 rows of
+    // X and Y when the last pass also gathers V); the last pass also writes the permuted copies (A6).  Measured
+    // (ncu, HunyuanVideo): the register-staged pass read X at 2.75 TB/s (register-limited occupancy), this one at ~4.5
     const bool gather = it + 1 == iters && g.Xp;
-    const int R = gather ? (g.Y.p ? 32 : 64) : kSumRows;
+    const bool two = gather && g.Y.p;
+    const int R = two ? 32 : 64;
     SegOut seg{ws.c_sum, ws.c_part, objective ? ws.c_sq : nullptr, ws.c_sqpart, (N + R - 1) / R};
-    if (gather) {
-      const dim3 grid_a((N + R * kAsyncWarps - 1) / (R * kAsyncWarps), BH);
-      const size_t sm = size_t(kAsyncWarps) * kAsyncRowBytes;
-      auto kern = g.Y.p ? (objective ? k_update_sum_async<D, true, 32> : k_update_sum_async<D, false, 32>)
-                        : (objective ? k_update_sum_async<D, true, 64> : k_update_sum_async<D, false, 64>);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-      kern<<<grid_a, 32 * kAsyncWarps, sm, s>>>(X, N, C, perm, labels, offsets, seg, static_cast<__nv_bfloat16*>(g.Xp),
-                                                g.Y, static_cast<__nv_bfloat16*>(g.Yp));
-    } else {
-      const dim3 grid_sum((N + kSumRows * kSumWarps - 1) / (kSumRows * kSumWarps), BH);
-      auto kern = objective ? k_update_sum<D, true> : k_update_sum<D, false>;
-      kern<<<grid_sum, 32 * kSumWarps, 0, s>>>(X, N, C, perm, labels, offsets, seg);
-    }
+    const dim3 grid_a((N + R * kAsyncWarps - 1) / (R * kAsyncWarps), BH);
+    const size_t sm = size_t(kAsyncWarps) * kAsyncRowBytes;
+    auto kern = two ? (objective ? k_update_sum_async<D, true, 32> : k_update_sum_async<D, false, 32>)
+                    : (objective ? k_update_sum_async<D, true, 64> : k_update_sum_async<D, false, 64>);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    kern<<<grid_a, 32 * kAsyncWarps, sm, s>>>(X, N, C, perm, labels, offsets, seg,
+                                              gather ? static_cast<__nv_bfloat16*>(g.Xp) : nullptr,
+                                              two ? g.Y : XView(), two ? static_cast<__nv_bfloat16*>(g.Yp) : nullptr);
     k_update_mean<D><<<dim3(C, BH), D, 0, s>>>(C, R, offsets, seg, cent, objective ? ws.j_part : nullptr);
     if (objective) k_objective<<<(BH + 127) / 128, 128, 0, s>>>(BH, C, ws.j_part, objective + size_t(it) * BH * 2);
   }
