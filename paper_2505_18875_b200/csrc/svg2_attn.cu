@@ -122,7 +122,7 @@ struct Params {
 // Measurement build only (-DSVG2_TRACE, tools/trace_attn.py): clock64 per event and key tile of the first item of
 // CTA 0, printed at kernel exit.  The product build compiles no trace code.
 #ifdef SVG2_TRACE
-constexpr int kTrT = 48, kTrEv = 16;
+constexpr int kTrT = 48, kTrEv = 24;
 __device__ long long g_trace[kTrEv][kTrT];
 #define TRACE(ev, t)                                                                       \
   do {                                                                                     \
@@ -513,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           negm += ld_shared_volatile(&zero_slot);  // every exponential depends on a load after the barrier
         }
         const uint64_t sl2x2 = f2(sl2, sl2), negm2 = f2(negm, negm);
+        if (g == 0) TRACE(20 + (warp & 3), t);  // exponential phase start, each warp of tile a
         uint64_t lsum2 = f2(0.f, 0.f);
         uint32_t pk[kN / 2];
 #pragma unroll
@@ -543,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.p_full[g]);
         if ((warp & 3) == 0) TRACE(12 + g, t);
+        if (g == 0) TRACE(16 + (warp & 3), t);  // P stored, each warp of tile a
         float ls0, ls1;
         f2_split(lsum2, ls0, ls1);
         l += ls0 + ls1;

@@ -18,7 +18,7 @@ import paper_2505_18875_b200 as svg2  # noqa: E402
 import svg2_synth  # noqa: E402
 
 EV = ["prodK", "prodV", "S_a", "S_b", "PV_a", "PV_b", "sfull_a", "sfull_b", "ld_a", "ld_b", "exp_a", "exp_b",
-      "pfull_a", "pfull_b", "max_a", "max_b"]
+      "pfull_a", "pfull_b", "max_a", "max_b", "P_a0", "P_a1", "P_a2", "P_a3", "E_a0", "E_a1", "E_a2", "E_a3"]
 wl = svg2_synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "hunyuan720p"]
 nh = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 q, k, v = svg2_synth.generate(wl, heads=range(nh))
@@ -28,9 +28,9 @@ for _ in range(2):
     svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, wl.top_p, ex["q_centroids"], ex["k_centroids"], warm=True)
 torch.cuda.synchronize()
 lib = svg2.load_library()
-buf = (ctypes.c_longlong * (16 * 48))()
+buf = (ctypes.c_longlong * (24 * 48))()
 assert lib.svg2_trace_dump(buf) == 0
-tr = np.array(buf, dtype=np.int64).reshape(16, 48)
+tr = np.array(buf, dtype=np.int64).reshape(24, 48)
 t0 = tr[0, 0]
 print("cycles relative to the first K issue; per key tile t (80 keys)")
 print("t   " + " ".join(f"{e:>8}" for e in EV))
@@ -43,3 +43,13 @@ d = np.diff(tr[6, 1:40])
 print("softmax a period (median cycles per tile):", float(np.median(d[d > 0])) if (d > 0).any() else None)
 d = np.diff(tr[2, 1:40])
 print("S_a issue period:", float(np.median(d[d > 0])) if (d > 0).any() else None)
+
+P = tr[16:20, 1:40].astype(np.float64)
+E = tr[20:24, 1:40].astype(np.float64)
+ok = (P > 0).all(0) & (E > 0).all(0)
+print("tile a, per tile: spread of P-stored times over the 4 warps (median, p90):",
+      float(np.median(P[:, ok].max(0) - P[:, ok].min(0))), float(np.quantile(P[:, ok].max(0) - P[:, ok].min(0), 0.9)))
+print("exp phase length per warp (median):", [float(np.median((P - E)[w, ok])) for w in range(4)])
+pv = tr[4, 1:40].astype(np.float64)
+okp = ok & (pv > 0)
+print("PV_a issue after the last warp's P (median cycles):", float(np.median(pv[okp] - P[:, okp].max(0))))
