@@ -224,6 +224,9 @@ cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_off
 cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void* Vp, int BH, int Nq, int Nk, int d,
                                       float scale, const int32_t* q_perm, const OutView& out, float* lse, AttnWs ws,
                                       cudaStream_t s, const uint32_t* v_amax = nullptr);
+// top_p = 1: every query cluster selects every non-empty key cluster, so the attention of a head is one query range
+// [0, Nq) over the whole key stream: q_offsets [BH, 2] = {0, Nq}, mask [BH, Ck] = 1 (no per-cluster Q-tile padding)
+cudaError_t launch_dense_stream(int BH, int Nq, int Ck, int32_t* q_offsets, uint8_t* mask, cudaStream_t s);
 int kmeans_launch_count(int iters, bool warm, bool objective = false);
 cudaError_t launch_kmeanspp(XView X, int BH, int N, int d, int C, uint32_t seed, int role, int bh_base,
                             float* cent, void* ws, cudaStream_t s);

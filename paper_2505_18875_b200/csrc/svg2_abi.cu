@@ -60,6 +60,8 @@ struct FusedWs {
   void *Qp, *Kp, *Vp;
   uint8_t* mask;
   double* scores;    // [BH, Cq, Ck] fp64 Eq. 1 scores of the selection
+  int32_t* dense_qoff;  // top_p = 1: [BH, 2] one query range per head
+  uint8_t* dense_mask;  // top_p = 1: [BH, Ck] all key clusters
   uint32_t* v_amax;  // FP8 PV: per-(head, channel) max |V| (f32 bits) [BH, d]
   KmeansWs km_q, km_k;  // per-role k-means scratch: the two roles may run concurrently
   AttnWs attn;
@@ -81,6 +83,8 @@ FusedWs carve_fused(Carver& c, const svg2_dims_t& dm, const svg2_config_t& cfg) 
   w.Vp = c.take<uint16_t>(BH * dm.Nk * dm.d);
   w.mask = c.take<uint8_t>(BH * cfg.Cq * cfg.Ck);
   w.scores = c.take<double>(select_ws_elems(int(BH), cfg.Cq, cfg.Ck));
+  w.dense_qoff = c.take<int32_t>(BH * 2);
+  w.dense_mask = c.take<uint8_t>(BH * cfg.Ck);
   w.v_amax = c.take<uint32_t>(BH * dm.d);
   w.km_q = carve_kmeans(c, int(BH), dm.Nq, cfg.Cq);
   w.km_k = carve_kmeans(c, int(BH), dm.Nk, cfg.Ck);
@@ -208,10 +212,15 @@ cudaError_t run_fused(const XView& Q, const XView& K, const XView& V, const svg2
     e = launch_select_topp(q_centroids, k_centroids, w.size_q, w.size_k, BH, cfg->Cq, cfg->Ck, dm.d, scale,
                            cfg->top_p, w.mask, selected_pairs, w.scores, s);
   mark(4);
+  // top_p = 1 (and no query-cluster split): every query cluster selects every non-empty key cluster (R11), so the
+  // attention runs each head as one query range over the whole key stream -- the same key order and the same result
+  // up to the lazy-rescale points, without the per-cluster Q-tile padding (W480p: tile work 1.19 -> 1.00)
+  const bool dense = cfg->top_p >= 1.0 && part.count == 1;
+  if (e == cudaSuccess && dense) e = launch_dense_stream(BH, dm.Nq, cfg->Ck, w.dense_qoff, w.dense_mask, s);
   if (e == cudaSuccess)
-    e = launch_build_worklist(w.off_q, w.off_k, w.mask, BH, dm.Nq, dm.Nk, cfg->Cq, cfg->Ck,
-                              attn_groups_per_tile(dm.d, fp8), w.attn, OrphanFill{w.perm_q, out, nullptr, dm.d}, s,
-                              part);
+    e = launch_build_worklist(dense ? w.dense_qoff : w.off_q, w.off_k, dense ? w.dense_mask : w.mask, BH, dm.Nq,
+                              dm.Nk, dense ? 1 : cfg->Cq, cfg->Ck, attn_groups_per_tile(dm.d, fp8), w.attn,
+                              OrphanFill{w.perm_q, out, nullptr, dm.d}, s, part);
   mark(5);
   if (e == cudaSuccess)
     e = launch_varblock_attention(w.Qp, w.Kp, w.Vp, BH, dm.Nq, dm.Nk, dm.d, scale, w.perm_q, out, nullptr, w.attn, s,
@@ -453,7 +462,8 @@ int32_t svg2_sparse_attention_launch_count(svg2_dims_t dm, const svg2_config_t* 
   if (!cfg) return 0;
   const bool warm = cfg->flags & SVG2_WARM_START;
   // the Q / K / V gathers are fused into the last k-means update (no launches of their own)
-  int n = 2 * kmeans_launch_count(cfg->iters, warm) + 1 /*select*/ + kWorklistLaunches + 1 /*attn*/;
+  int n = 2 * kmeans_launch_count(cfg->iters, warm) + 2 /*scores + select*/ + kWorklistLaunches + 1 /*attn*/;
+  if (cfg->top_p >= 1.0) n += 1;  // the dense stream's query offsets (the mask is a memset)
   if (cfg->flags & SVG2_FP8_PV) n += 2;  // |V| max per head + the e4m3 gather
   if (!warm && (cfg->flags & SVG2_INIT_KMEANSPP))
     n += kmeanspp_launch_count(dm.B * dm.H, dm.Nq, dm.d) + kmeanspp_launch_count(dm.B * dm.H, dm.Nk, dm.d) - 2;

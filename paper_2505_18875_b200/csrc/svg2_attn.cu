@@ -936,8 +936,22 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
 
 }  // namespace
 
+__global__ void k_dense_qoff(int BH, int Nq, int32_t* __restrict__ q_offsets) {
+  const int bh = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bh < BH) {
+    q_offsets[2 * bh] = 0;
+    q_offsets[2 * bh + 1] = Nq;
+  }
+}
+
 static_assert(Cfg<128>::kGpt >= kMinGroupsPerTile && Cfg<64>::kGpt >= kMinGroupsPerTile, "tile_cap");
 int attn_groups_per_tile(int d, bool fp8) { return fp8 ? kKTile / 8 : (d == 128 ? Cfg<128>::kGpt : Cfg<64>::kGpt); }
+
+cudaError_t launch_dense_stream(int BH, int Nq, int Ck, int32_t* q_offsets, uint8_t* mask, cudaStream_t s) {
+  k_dense_qoff<<<(BH + 127) / 128, 128, 0, s>>>(BH, Nq, q_offsets);
+  cudaMemsetAsync(mask, 1, size_t(BH) * Ck, s);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask, int BH,
                                   int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s,
