@@ -21,11 +21,12 @@ EV = ["prodK", "prodV", "S_a", "S_b", "PV_a", "PV_b", "sfull_a", "sfull_b", "ld_
       "pfull_a", "pfull_b", "max_a", "max_b", "P_a0", "P_a1", "P_a2", "P_a3", "E_a0", "E_a1", "E_a2", "E_a3"]
 wl = svg2_synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "hunyuan720p"]
 nh = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+top_p = float(sys.argv[3]) if len(sys.argv) > 3 else wl.top_p
 q, k, v = svg2_synth.generate(wl, heads=range(nh))
 Q, K, V = (torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).cuda() for a in (q, k, v))
-O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, wl.top_p)
+O, pairs, ex = svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, wl.iters, top_p)
 for _ in range(2):
-    svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, wl.top_p, ex["q_centroids"], ex["k_centroids"], warm=True)
+    svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, top_p, ex["q_centroids"], ex["k_centroids"], warm=True)
 torch.cuda.synchronize()
 lib = svg2.load_library()
 buf = (ctypes.c_longlong * (24 * 48))()
