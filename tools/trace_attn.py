@@ -12,7 +12,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-LIB = os.path.join(ROOT, "build", "libsvg2_trace.so")
+LIB = os.environ.get("SVG2_TRACE_LIB", os.path.join(ROOT, "build", "libsvg2_trace.so"))
 os.environ["SVG2_LIBRARY"] = LIB
 import paper_2505_18875_b200 as svg2  # noqa: E402
 import svg2_synth  # noqa: E402
