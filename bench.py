@@ -426,7 +426,40 @@ def run_ours(args, wl):
     # ---- e2e through the C-ABI call on HOST buffers (svg2_sparse_attention_host, rank-local heads): every step moves
     # this rank's Q, K, V from pinned host memory to the device and O back, inside the library's pipeline
     e2e = None
-    if pinned is not None:
+    if pinned is not None and world > 1 and assignment is None:
+        # N > 1: what a sequence-parallel caller does per step -- its token shard of Q, K, V [B, N/P, H, d] from pinned
+        # host memory to the device, the Ulysses reshard in (overlapped with the k-means, input-ready events), the
+        # fused call on this rank's heads, the reshard out, and its O shard back to pinned host memory
+        hs = [t.cpu().pin_memory() for t in (Qs, Ks, Vs)]
+        ds = [torch.empty_like(t) for t in (Qs, Ks, Vs)]
+        o_host = torch.empty(tuple(Qs.shape), dtype=torch.bfloat16).pin_memory()
+        qc_e, kc_e = cq.clone(), ck.clone()
+        comm_e = torch.cuda.Stream()
+
+        def e2e_step():
+            for dd, hh in zip(ds, hs):
+                dd.copy_(hh, non_blocking=True)
+            (Qh, Kh, Vh), ready = seq_to_head_overlapped(tuple(ds), comm_e)
+            Oh, _, _ = svg2.sparse_attention(Qh, Kh, Vh, wl.Cq, wl.Ck, iters_w, top_p, qc_e, kc_e, warm=True, fp8=fp8,
+                                             input_ready=ready)
+            o_host.copy_(head_to_seq(Oh), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s3.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e3.record()
+        torch.cuda.synchronize()
+        te = reduce_scalar(s3.elapsed_time(e3) / args.steps, "max")
+        nbytes = int(reduce_scalar(float(Qs.numel() * 2), "sum"))
+        e2e = {"value": dense_flops / (te * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": te,
+               "h2d_bytes_per_step": 3 * nbytes, "d2h_bytes_per_step": nbytes,
+               "api": "token shards from pinned host -> Ulysses all-to-all (dist.seq_to_head_overlapped) -> "
+                      "sparse_attention -> all-to-all back -> pinned host"}
+    elif pinned is not None:
         out_host = torch.empty((B, Hl, N, d), dtype=torch.bfloat16).pin_memory()
         qc_e, kc_e = cq.clone(), ck.clone()
 
