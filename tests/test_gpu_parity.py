@@ -351,6 +351,38 @@ def test_fused_stagewise(svg2, oracle_mod, case):
     check_attention(O[0, 0], ref, case)
 
 
+@pytest.mark.parametrize("B,H,Nq,Nk,d,Cq,Ck", [(2, 2, 3000, 4100, 128, 24, 60), (1, 3, 5000, 2000, 64, 40, 33)])
+def test_fused_cross_shapes_stagewise(svg2, oracle_mod, B, H, Nq, Nk, d, Cq, Ck):
+    """The fused call with Nq != Nk (cross-attention shapes), B > 1 and d = 64 / 128, stage by stage against the oracle:
+    k-means of both roles (cold strided, labels within R16 and, where no flip occurred, bit-exact sizes and
+    centroids), permutations and offsets bit-exact, mask within R17 with exact pair counts, attention on every row."""
+    q, k, v = random_qkv(B, H, Nq, Nk, d, seed=Nq + Nk, groups=14)
+    Q, K, V = to_dev(q), to_dev(k), to_dev(v)
+    O, pairs, ex = svg2.sparse_attention(Q, K, V, Cq, Ck, 3, 0.9, debug=True)
+    torch.cuda.synchronize()
+    Q64, K64, V64 = to_f64(Q), to_f64(K), to_f64(V)
+    for b in range(B):
+        for h in range(H):
+            for X64, C, key in ((Q64[b, h], Cq, "q"), (K64[b, h], Ck, "k")):
+                gl = ex[f"{key}_labels"].cpu().numpy()[b, h]
+                ol, oc, osz = oracle_mod.kmeans(X64, C, 3)
+                if np.array_equal(gl, ol):
+                    assert np.array_equal(ex[f"{key}_centroids"].cpu().numpy()[b, h], oc.astype(np.float32))
+                p_ref, o_ref = oracle_mod.permute(gl, C)
+                assert np.array_equal(ex[f"{key}_perm"].cpu().numpy()[b, h], p_ref)
+                assert np.array_equal(ex[f"{key}_offsets"].cpu().numpy()[b, h], o_ref)
+            lq, lk, m = (ex[n].cpu().numpy()[b, h] for n in ("q_labels", "k_labels", "mask"))
+            sq, sk = np.bincount(lq, minlength=Cq), np.bincount(lk, minlength=Ck)
+            om, opairs, S, W, Z = oracle_mod.select_topp(ex["q_centroids"].cpu().numpy()[b, h].astype(np.float64),
+                                                         ex["k_centroids"].cpu().numpy()[b, h].astype(np.float64),
+                                                         sq, sk, d, f32scale(d), 0.9, return_tables=True)
+            nrows, nontie = mask_mismatch_rows_are_ties(W, Z, sk, 0.9, m, om)
+            assert nontie == 0
+            assert int(pairs[b, h]) == int((sq[:, None] * sk[None, :] * m).sum())
+            ref = oracle_mod.attention_rows(Q64[b, h], K64[b, h], V64[b, h], f32scale(d), lq=lq, lk=lk, mask=m)
+            check_attention(O[b, h], ref, f"b{b} h{h}")
+
+
 # ------------------------------------------------------------------ P7 and special cases
 @pytest.mark.parametrize("shape", [(1, 1, 1024, 1024, 64), (1, 2, 3000, 3000, 128)])
 def test_p1_equals_dense(svg2, oracle_mod, shape):
