@@ -1,6 +1,7 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every entry point of libsvg2.so on
 the tiny config and on a reduced-N HunyuanVideo shape (N = 6000, 2 heads, d = 128, Cq/Ck = 100/500), cold (strided and
-k-means++) and warm, bf16 and FP8 PV, the standalone stages, the host-buffer pipeline and the objective output.
+k-means++) and warm, bf16 and FP8 PV, the standalone stages, the host-buffer pipeline, the objective output, and the
+layout entry (strided inputs, token-sharded outputs, query-cluster parts, p = 1).
     compute-sanitizer --tool memcheck python tools/sanitize_driver.py
 """
 import dataclasses
@@ -35,6 +36,18 @@ def run(wl, fp8):
     svg2.unpermute(Op, pq)
     Qh, Kh, Vh = (t.cpu().pin_memory() for t in (Q, K, V))
     svg2.sparse_attention_host(Qh, Kh, Vh, wl.Cq, wl.Ck, 2, wl.top_p)
+    # svg2_sparse_attention_layout: token-major strided inputs, output rows into 2 token shards, query-cluster parts,
+    # and the p = 1 dense stream
+    Qt, Kt, Vt = (t.permute(0, 2, 1, 3).contiguous().permute(0, 2, 1, 3) for t in (Q, K, V))
+    B, H, N, d = Q.shape
+    n = (N + 1) // 2
+    shards = [torch.zeros(B, n, H, d, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    t0 = shards[0]
+    for part in ((0, 2), (1, 2)):
+        svg2.sparse_attention(Qt, Kt, Vt, wl.Cq, wl.Ck, 2, wl.top_p, part=part,
+                              out_shards=dict(shards=shards, shard_tokens=n,
+                                              strides=(t0.stride(0), t0.stride(2), t0.stride(1)), head_offset=0))
+    svg2.sparse_attention(Q, K, V, wl.Cq, wl.Ck, 2, 1.0)
     torch.cuda.synchronize()
     print(f"{wl.name}: ok, density {float(pairs.double().mean()) / (wl.N * wl.N):.3f}", flush=True)
 
