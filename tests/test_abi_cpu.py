@@ -98,6 +98,55 @@ def test_validation_rejects_before_touching_the_device(lib):
                                      fake, None, None, fake, 1 << 30, None) == 2
 
 
+def test_layout_validation(lib):
+    """svg2_sparse_attention_layout rejects bad layouts synchronously (before any device call): strides that are not
+    positive multiples of 8 elements or shorter than a row, more than 16 output shards, shards that do not cover Nq,
+    a NULL shard pointer, a misaligned shard, bad query-cluster part ranges, and an aux stream without its events."""
+    import paper_2505_18875_b200 as m
+    cfg = m.Config(8, 8, 1, 0.9, 0.0, 0)
+    dims = m.Dims(1, 2, 256, 256, 64)
+    fake = ctypes.c_void_p(0x10000)
+
+    def call(lay, O=fake):
+        return lib.svg2_sparse_attention_layout(fake, fake, fake, dims, ctypes.byref(cfg), ctypes.byref(lay), fake,
+                                                fake, O, None, None, None, fake, 1 << 30, None)
+
+    def layout(**kw):
+        lay = m.Layout()
+        for k, v in kw.items():
+            if k.endswith("strides"):
+                getattr(lay, k)[:] = v
+            else:
+                setattr(lay, k, v)
+        return lay
+
+    assert call(layout(q_strides=(256 * 2 * 64, 64, 2 * 64 + 4))) == 2  # sN not a multiple of 8
+    assert call(layout(k_strides=(256 * 2 * 64, 64, 32))) == 2           # sN < d
+    assert call(layout(v_strides=(0, 64, 128))) == 2                     # partly zero
+    assert call(layout(part_begin=0, part_end=3, part_count=2)) == 3     # end > count
+    assert call(layout(part_begin=1, part_end=1, part_count=2)) == 3     # empty range
+    assert call(layout(part_begin=0, part_end=1, part_count=5000)) == 3  # count > 4096
+    shards = (ctypes.c_void_p * 17)(*([0x10000] * 17))
+    too_many = layout(o_shards=ctypes.cast(shards, ctypes.c_void_p), n_shards=17, shard_tokens=16,
+                      o_strides=(16 * 2 * 64, 64, 128))
+    assert call(too_many, O=None) == 2
+    short = layout(o_shards=ctypes.cast(shards, ctypes.c_void_p), n_shards=2, shard_tokens=100,
+                   o_strides=(100 * 2 * 64, 64, 128))
+    assert call(short, O=None) == 2                                       # 2 x 100 < 256 tokens
+    nulls = (ctypes.c_void_p * 2)(0x10000, None)
+    with_null = layout(o_shards=ctypes.cast(nulls, ctypes.c_void_p), n_shards=2, shard_tokens=128,
+                       o_strides=(128 * 2 * 64, 64, 128))
+    assert call(with_null, O=None) == 1
+    odd = (ctypes.c_void_p * 2)(0x10000, 0x10008)
+    misaligned = layout(o_shards=ctypes.cast(odd, ctypes.c_void_p), n_shards=2, shard_tokens=128,
+                        o_strides=(128 * 2 * 64, 64, 128))
+    assert call(misaligned, O=None) == 4
+    assert call(layout(aux_stream=0x1234)) == 1                           # aux stream without its events
+    # a valid layout passes validation (then fails later on the fake pointers, never with a layout status)
+    ok = layout(q_strides=(256 * 2 * 64, 64, 128), part_begin=0, part_end=1, part_count=2)
+    assert call(ok) not in (1, 2, 3, 4, 5)
+
+
 def test_sass_has_tcgen05_and_tma(lib):
     """The attention and the permutation path compile to Blackwell-native instructions (UTCHMMA, UTMALDG, LDTM)."""
     import subprocess
