@@ -32,7 +32,7 @@ struct AsgCfg {
   static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;  // 128 rows x D bf16
   static constexpr uint32_t kNormBytes = kMaxClusters * 4;
   // X: 2 buffers | centroid chunk stages: 2 x (hi tile + lo tile) | norms
-  static constexpr uint32_t kSmem = 2 * kTileBytes + 4 * kTileBytes + kNormBytes + 1024;
+  static constexpr uint32_t kSmem = 2 * kTileBytes + 4 * kTileBytes + kNormBytes + 1024;  // X x2 | 4 half-chunks
 };
 
 template <int D>
@@ -57,8 +57,13 @@ __global__ void __launch_bounds__(D) k_centroid_split(const float* __restrict__ 
   }
 }
 
+// centroid ring: kHalfStages half-stages, each one tile (the hi or the lo half of a 128-centroid chunk), so the hi
+// half of chunk c+1 streams in while the lo half of chunk c is multiplied (a 2-deep ring of whole hi+lo chunks left the
+// MMA waiting for chunks ~30% of the time: tensor pipe 68%, ncu)
+constexpr int kHalfStages = 4;
 struct AsgBars {
-  uint64_t x_full[2], x_empty[2], c_full[2], c_empty[2], acc_full[kAccStages], acc_empty[kAccStages];
+  uint64_t x_full[2], x_empty[2], c_full[kHalfStages], c_empty[kHalfStages], acc_full[kAccStages],
+      acc_empty[kAccStages];
 };
 
 // Persistent assignment: one CTA per SM walks a contiguous range of 128-row work units (row tiles of one (b,h); the
@@ -75,9 +80,8 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sX = smem;                       // [2 buffers]
-  uint8_t* sH = smem + 2 * C::kTileBytes;   // [2 stages]
-  uint8_t* sL = sH + 2 * C::kTileBytes;     // [2 stages]
-  float* sNorm = reinterpret_cast<float*>(sL + 2 * C::kTileBytes);  // [Cpad] of the epilogue's current head
+  uint8_t* sC = smem + 2 * C::kTileBytes;   // [kHalfStages] centroid half-chunks (hi or lo)
+  float* sNorm = reinterpret_cast<float*>(sC + kHalfStages * C::kTileBytes);  // [Cpad] of the epilogue's current head
   __shared__ AsgBars bars;
   __shared__ uint32_t tmem_slot;
 
@@ -93,6 +97,8 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars.x_full[s], 1);
       mbar_init(&bars.x_empty[s], 1);
+    }
+    for (int s = 0; s < kHalfStages; ++s) {
       mbar_init(&bars.c_full[s], 1);
       mbar_init(&bars.c_empty[s], 1);
     }
@@ -110,8 +116,8 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      uint32_t cc = 0;
-      int held[2] = {-1, -1};  // head whose (single) centroid chunk a stage holds
+      uint32_t cc = 0;  // half-chunks issued
+      int held[kHalfStages] = {-1, -1, -1, -1};  // C <= 128: head whose centroid half a stage holds
       for (int u = u0, i = 0; u < u1; ++u, ++i) {
         const int bh = u / upb, row0 = (u - bh * upb) * kAsgRows;
         const int xs = i & 1;
@@ -120,19 +126,20 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         for (int b = 0; b < C::kBlocks; ++b)
           tma_load_4d(sX + xs * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full[xs], 64 * b, row0, bh % H,
                       bh / H);
-        for (int c = 0; c < nchunks; ++c, ++cc) {
-          const int s = cc & 1;
-          mbar_wait(&bars.c_empty[s], ((cc >> 1) & 1) ^ 1);
-          if (nchunks == 1 && held[s] == bh) {  // C <= 128: the stage still holds this head's centroids
-            mbar_arrive(&bars.c_full[s]);
-            continue;
-          }
-          if (nchunks == 1) held[s] = bh;
-          mbar_arrive_expect_tx(&bars.c_full[s], 2 * C::kTileBytes);
+        for (int c = 0; c < nchunks; ++c) {
           const int crow = bh * Cpad + c * kCentChunk;
-          for (int b = 0; b < C::kBlocks; ++b) {
-            tma_load_2d(sH + s * C::kTileBytes + b * C::kBlockBytes, &mapHi, &bars.c_full[s], 64 * b, crow);
-            tma_load_2d(sL + s * C::kTileBytes + b * C::kBlockBytes, &mapLo, &bars.c_full[s], 64 * b, crow);
+          for (int half = 0; half < 2; ++half, ++cc) {  // hi, then lo
+            const int s = cc % kHalfStages;
+            mbar_wait(&bars.c_empty[s], ((cc / kHalfStages) & 1) ^ 1);
+            if (nchunks == 1 && held[s] == bh) {  // C <= 128: the stage still holds this head's half
+              mbar_arrive(&bars.c_full[s]);
+              continue;
+            }
+            if (nchunks == 1) held[s] = bh;
+            mbar_arrive_expect_tx(&bars.c_full[s], C::kTileBytes);
+            for (int b = 0; b < C::kBlocks; ++b)
+              tma_load_2d(sC + s * C::kTileBytes + b * C::kBlockBytes, half ? &mapLo : &mapHi, &bars.c_full[s],
+                          64 * b, crow);
           }
         }
       }
@@ -145,24 +152,22 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
       const int xs = i & 1;
       mbar_wait_warp(&bars.x_full[xs], (i >> 1) & 1);
       const uint32_t x = smem_u32(sX + xs * C::kTileBytes);
-      for (int c = 0; c < nchunks; ++c, ++cc, ++ac) {
-        const int s = cc & 1, as = ac % kAccStages;
-        mbar_wait_warp(&bars.c_full[s], (cc >> 1) & 1);
+      for (int c = 0; c < nchunks; ++c, ++ac) {
+        const int as = ac % kAccStages;
         mbar_wait_warp(&bars.acc_empty[as], ((ac / kAccStages) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t h = smem_u32(sH + s * C::kTileBytes), l = smem_u32(sL + s * C::kTileBytes);
         const uint32_t dcol = tmem + as * 128;
+        for (int half = 0; half < 2; ++half, ++cc) {  // x.hi then x.lo into the same accumulator
+          const int s = cc % kHalfStages;
+          mbar_wait_warp(&bars.c_full[s], (cc / kHalfStages) & 1);
+          tc_fence_after();
+          const uint32_t cb = smem_u32(sC + s * C::kTileBytes);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
-          mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(h + off), idesc, k > 0);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+            mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(cb + off), idesc, (half | k) > 0);
+          }
+          mma_commit_warp(&bars.c_empty[s]);
         }
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
-          mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(l + off), idesc, 1u);
-        }
-        mma_commit_warp(&bars.c_empty[s]);
         mma_commit_warp(&bars.acc_full[as]);
       }
       mma_commit_warp(&bars.x_empty[xs]);
@@ -180,8 +185,18 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         named_bar_sync(1, 128);
         cur_bh = bh;
       }
-      float best = INFINITY;
-      int bj = 0;
+      // kChains independent running argmins (column e of every 32 goes to chain e % kChains, indices ascending within
+      // a chain, strict < keeps the lowest), merged at the end by (distance, index): the same label as one sequential
+      // scan, without its compare-select dependency chain (ncu: the epilogue's serial argmin was the assign kernel's
+      // hot spot, 60% of samples, "wait" stalls 37%)
+      constexpr int kChains = 4;
+      float best[kChains];
+      int bj[kChains];
+#pragma unroll
+      for (int k = 0; k < kChains; ++k) {
+        best[k] = INFINITY;
+        bj[k] = 0;
+      }
       for (int c = 0; c < nchunks; ++c, ++ac) {
         const int as = ac % kAccStages;
         mbar_wait(&bars.acc_full[as], (ac / kAccStages) & 1);
@@ -194,12 +209,19 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
 #pragma unroll
         for (int q = 0; q < kCentChunk / 32; ++q) {
           const int j0 = c * kCentChunk + 32 * q;
+          const float4* nv = reinterpret_cast<const float4*>(sNorm + j0);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float dist = fmaf(-2.f, __uint_as_float(r4[q][e]), sNorm[j0 + e]);
-            if (dist < best) {  // strict: ties keep the lower index
-              best = dist;
-              bj = j0 + e;
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 n4 = nv[e4];  // broadcast 16-byte load of four norms
+            const float nn[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int e = 4 * e4 + k;
+              const float dist = fmaf(-2.f, __uint_as_float(r4[q][e]), nn[k]);
+              if (dist < best[k]) {  // strict: ties keep the lower index
+                best[k] = dist;
+                bj[k] = j0 + e;
+              }
             }
           }
         }
@@ -208,8 +230,17 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.acc_empty[as]);
       }
+      float b = best[0];
+      int jb = bj[0];
+#pragma unroll
+      for (int k = 1; k < kChains; ++k) {
+        if (best[k] < b || (best[k] == b && bj[k] < jb)) {
+          b = best[k];
+          jb = bj[k];
+        }
+      }
       const int row = row0 + quarter * 32 + lane;
-      if (row < N) labels[size_t(bh) * N + row] = bj;
+      if (row < N) labels[size_t(bh) * N + row] = jb;
     }
   }
   tc_fence_before();
