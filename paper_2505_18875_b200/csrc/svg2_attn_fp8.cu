@@ -25,7 +25,7 @@
 
 namespace svg2 {
 namespace {
-// (internal names shared with svg2_attn3.cu live in this file's anonymous namespace)
+// (its helpers live in this file's anonymous namespace; the bf16 pipeline is svg2_attn.cu)
 
 constexpr int kThreads = 384;
 constexpr int kStages = 2;     // K/V ring depth (bf16)
