@@ -106,13 +106,13 @@ struct KmeansWs {
   uint16_t* c_lo;     // [BH, Cpad, d] bf16 lo part: c - hi
   float* c_norm;      // [BH, Cpad]  ||c||^2 (f32), +inf for padding centroids
   double* c_sum;      // [BH, C, d]  fp64 sums of the clusters that lie inside one update chunk
-  double* c_part;     // [BH, ceil(N/kUpdMinRows), 2, d]  fp64 chunk partials of clusters crossing chunk boundaries
+  double* c_part;     // [BH, ceil(N/kUpdRows), 2, d]  fp64 chunk partials of clusters crossing chunk boundaries
   double* c_sq;       // [BH, C]  (objective) sum ||x||^2 per cluster, as c_sum
-  double* c_sqpart;   // [BH, ceil(N/kUpdMinRows), 2]
+  double* c_sqpart;   // [BH, ceil(N/kUpdRows), 2]
   double* j_part;     // [BH, C, 2]  (objective) per-cluster J before / after the update
   void* pp;           // k-means++ seeding scratch (kmeanspp_ws_bytes)
 };
-constexpr int kUpdMinRows = 32;  // the smallest update chunk (rows per warp) of the segmented centroid reduction
+constexpr int kUpdRows = 32;  // rows per chunk (one warp) of the segmented centroid reduction
 constexpr int kPPMaxBlocks = 64;  // k-means++: CTAs per head
 size_t kmeanspp_ws_bytes(int BH, int N);
 inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
@@ -124,7 +124,7 @@ inline KmeansWs carve_kmeans(Carver& c, int BH, int N, int C, int d = 128) {
   w.c_lo = c.take<uint16_t>(size_t(BH) * cent_pad(C) * d);
   w.c_norm = c.take<float>(size_t(BH) * cent_pad(C));
   w.c_sum = c.take<double>(size_t(BH) * C * d);
-  const size_t nch = (size_t(N) + kUpdMinRows - 1) / kUpdMinRows;
+  const size_t nch = (size_t(N) + kUpdRows - 1) / kUpdRows;
   w.c_part = c.take<double>(size_t(BH) * nch * 2 * d);
   w.c_sq = c.take<double>(size_t(BH) * C);
   w.c_sqpart = c.take<double>(size_t(BH) * nch * 2);

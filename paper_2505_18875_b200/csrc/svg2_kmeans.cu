@@ -24,6 +24,7 @@ namespace {
 constexpr int kAsgThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 argmin epilogue (one TMEM lane quarter each)
 constexpr int kAsgRows = 128;     // rows per work unit (one M = 128 tile)
 constexpr int kAccStages = 4;     // TMEM accumulator stages of 128 columns
+constexpr int kTiles = 6;         // shared-memory tiles of 128 rows x D, split between X buffers and centroid stages
 
 template <int D>
 struct AsgCfg {
@@ -31,8 +32,8 @@ struct AsgCfg {
   static constexpr uint32_t kBlockBytes = 128 * 128;            // 128 rows x 64 bf16
   static constexpr uint32_t kTileBytes = kBlocks * kBlockBytes;  // 128 rows x D bf16
   static constexpr uint32_t kNormBytes = kMaxClusters * 4;
-  // X: 2 buffers | centroid chunk stages: 2 x (hi tile + lo tile) | norms
-  static constexpr uint32_t kSmem = 2 * kTileBytes + 4 * kTileBytes + kNormBytes + 1024;  // X x2 | 4 half-chunks
+  // six tiles (X buffers | centroid half-chunk stages) | norms
+  static constexpr uint32_t kSmem = kTiles * kTileBytes + kNormBytes + 1024;
 };
 
 template <int D>
@@ -57,13 +58,13 @@ __global__ void __launch_bounds__(D) k_centroid_split(const float* __restrict__ 
   }
 }
 
-// centroid ring: kHalfStages half-stages, each one tile (the hi or the lo half of a 128-centroid chunk), so the hi
-// half of chunk c+1 streams in while the lo half of chunk c is multiplied (a 2-deep ring of whole hi+lo chunks left the
-// MMA waiting for chunks ~30% of the time: tensor pipe 68%, ncu)
-constexpr int kHalfStages = 4;
+// The six tiles: kXS X buffers and kTiles - kXS centroid half-stages, each one tile (the hi or the lo half of a
+// 128-centroid chunk).  C > 128 (kXS = 2): four half-stages, so the hi half of chunk c+1 streams in while the lo half
+// of chunk c is multiplied (a 2-deep ring of whole hi+lo chunks left the MMA waiting for chunks ~30% of the time:
+// tensor pipe 68%, ncu).  C <= 128 (kXS = 4): one chunk, whose hi and lo halves stay resident across a head's units,
+// so two half-stages suffice and four X buffers keep more of the X stream in flight (the Q role reads X at HBM rate).
 struct AsgBars {
-  uint64_t x_full[2], x_empty[2], c_full[kHalfStages], c_empty[kHalfStages], acc_full[kAccStages],
-      acc_empty[kAccStages];
+  uint64_t x_full[4], x_empty[4], c_full[4], c_empty[4], acc_full[kAccStages], acc_empty[kAccStages];
 };
 
 // Persistent assignment: one CTA per SM walks a contiguous range of 128-row work units (row tiles of one (b,h); the
@@ -71,16 +72,18 @@ struct AsgBars {
 // stages, hi and lo tiles); the MMA warp accumulates X [hi | lo]^T per chunk into one of four TMEM stages; the
 // epilogue warps read each stage back and keep the running argmin.  Loads, MMAs and TMEM reads of consecutive
 // units overlap, and TMEM allocation / barrier setup happen once per CTA instead of once per tile.
-template <int D>
+template <int D, int kXS>
 __global__ void __launch_bounds__(kAsgThreads, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapHi,
                 const __grid_constant__ CUtensorMap mapLo, const float* __restrict__ c_norm, int N, int Cpad,
                 int BH, int H, int32_t* __restrict__ labels) {
   using C = AsgCfg<D>;
+  constexpr int kHalfStages = kTiles - kXS;
+  static_assert(kXS == 2 || kXS == 4, "X buffers");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sX = smem;                       // [2 buffers]
-  uint8_t* sC = smem + 2 * C::kTileBytes;   // [kHalfStages] centroid half-chunks (hi or lo)
+  uint8_t* sX = smem;                         // [kXS buffers]
+  uint8_t* sC = smem + kXS * C::kTileBytes;   // [kHalfStages] centroid half-chunks (hi or lo)
   float* sNorm = reinterpret_cast<float*>(sC + kHalfStages * C::kTileBytes);  // [Cpad] of the epilogue's current head
   __shared__ AsgBars bars;
   __shared__ uint32_t tmem_slot;
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
     tma_prefetch_desc(&mapX);
     tma_prefetch_desc(&mapHi);
     tma_prefetch_desc(&mapLo);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kXS; ++s) {
       mbar_init(&bars.x_full[s], 1);
       mbar_init(&bars.x_empty[s], 1);
     }
@@ -116,30 +119,42 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      uint32_t cc = 0;  // half-chunks issued
-      int held[kHalfStages] = {-1, -1, -1, -1};  // C <= 128: head whose centroid half a stage holds
+      uint32_t cc = 0;  // half-chunks issued (C > 128) / centroid loads (C <= 128)
+      int cur_bh = -1;
       for (int u = u0, i = 0; u < u1; ++u, ++i) {
         const int bh = u / upb, row0 = (u - bh * upb) * kAsgRows;
-        const int xs = i & 1;
-        mbar_wait(&bars.x_empty[xs], ((i >> 1) & 1) ^ 1);
+        const int xs = i % kXS;
+        mbar_wait(&bars.x_empty[xs], ((i / kXS) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars.x_full[xs], C::kTileBytes);
         for (int b = 0; b < C::kBlocks; ++b)
           tma_load_4d(sX + xs * C::kTileBytes + b * C::kBlockBytes, &mapX, &bars.x_full[xs], 64 * b, row0, bh % H,
                       bh / H);
-        for (int c = 0; c < nchunks; ++c) {
-          const int crow = bh * Cpad + c * kCentChunk;
-          for (int half = 0; half < 2; ++half, ++cc) {  // hi, then lo
-            const int s = cc % kHalfStages;
-            mbar_wait(&bars.c_empty[s], ((cc / kHalfStages) & 1) ^ 1);
-            if (nchunks == 1 && held[s] == bh) {  // C <= 128: the stage still holds this head's half
-              mbar_arrive(&bars.c_full[s]);
-              continue;
+        if constexpr (kXS == 4) {
+          // C <= 128: the head's hi and lo halves stay resident in stages 0 / 1; reloaded when the head changes,
+          // after the MMA released them (it commits c_empty after the head's last unit), so the X stream runs
+          // kXS units ahead of the MMA
+          if (bh != cur_bh) {
+            for (int half = 0; half < 2; ++half) {
+              mbar_wait(&bars.c_empty[half], (cc & 1) ^ 1);
+              mbar_arrive_expect_tx(&bars.c_full[half], C::kTileBytes);
+              for (int b = 0; b < C::kBlocks; ++b)
+                tma_load_2d(sC + half * C::kTileBytes + b * C::kBlockBytes, half ? &mapLo : &mapHi,
+                            &bars.c_full[half], 64 * b, bh * Cpad);
             }
-            if (nchunks == 1) held[s] = bh;
-            mbar_arrive_expect_tx(&bars.c_full[s], C::kTileBytes);
-            for (int b = 0; b < C::kBlocks; ++b)
-              tma_load_2d(sC + s * C::kTileBytes + b * C::kBlockBytes, half ? &mapLo : &mapHi, &bars.c_full[s],
-                          64 * b, crow);
+            ++cc;
+            cur_bh = bh;
+          }
+        } else {
+          for (int c = 0; c < nchunks; ++c) {
+            const int crow = bh * Cpad + c * kCentChunk;
+            for (int half = 0; half < 2; ++half, ++cc) {  // hi, then lo
+              const int s = cc % kHalfStages;
+              mbar_wait(&bars.c_empty[s], ((cc / kHalfStages) & 1) ^ 1);
+              mbar_arrive_expect_tx(&bars.c_full[s], C::kTileBytes);
+              for (int b = 0; b < C::kBlocks; ++b)
+                tma_load_2d(sC + s * C::kTileBytes + b * C::kBlockBytes, half ? &mapLo : &mapHi, &bars.c_full[s],
+                            64 * b, crow);
+            }
           }
         }
       }
@@ -148,27 +163,56 @@ __global__ void __launch_bounds__(kAsgThreads, 1)
     // whole warp, convergent: elect.sync inside the MMA asm -> back-to-back UTCHMMA on uniform registers
     const uint32_t idesc = idesc_bf16_f32(128, kCentChunk, false);
     uint32_t cc = 0, ac = 0;
+    int cur_bh = -1;
     for (int u = u0, i = 0; u < u1; ++u, ++i) {
-      const int xs = i & 1;
-      mbar_wait_warp(&bars.x_full[xs], (i >> 1) & 1);
+      const int xs = i % kXS;
+      mbar_wait_warp(&bars.x_full[xs], (i / kXS) & 1);
       const uint32_t x = smem_u32(sX + xs * C::kTileBytes);
-      for (int c = 0; c < nchunks; ++c, ++ac) {
+      if constexpr (kXS == 4) {
+        const int bh = u / upb;
+        if (bh != cur_bh) {  // this head's centroids were loaded (load number cc)
+          mbar_wait_warp(&bars.c_full[0], cc & 1);
+          mbar_wait_warp(&bars.c_full[1], cc & 1);
+          ++cc;
+          cur_bh = bh;
+        }
         const int as = ac % kAccStages;
         mbar_wait_warp(&bars.acc_empty[as], ((ac / kAccStages) & 1) ^ 1);
+        tc_fence_after();
         const uint32_t dcol = tmem + as * 128;
-        for (int half = 0; half < 2; ++half, ++cc) {  // x.hi then x.lo into the same accumulator
-          const int s = cc % kHalfStages;
-          mbar_wait_warp(&bars.c_full[s], (cc / kHalfStages) & 1);
-          tc_fence_after();
-          const uint32_t cb = smem_u32(sC + s * C::kTileBytes);
+        for (int half = 0; half < 2; ++half) {  // x.hi then x.lo into the same accumulator
+          const uint32_t cb = smem_u32(sC + half * C::kTileBytes);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
             mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(cb + off), idesc, (half | k) > 0);
           }
-          mma_commit_warp(&bars.c_empty[s]);
+        }
+        if (u + 1 == u1 || (u + 1) / upb != bh) {  // the head's last unit here: its centroid stages are free
+          mma_commit_warp(&bars.c_empty[0]);
+          mma_commit_warp(&bars.c_empty[1]);
         }
         mma_commit_warp(&bars.acc_full[as]);
+        ++ac;
+      } else {
+        for (int c = 0; c < nchunks; ++c, ++ac) {
+          const int as = ac % kAccStages;
+          mbar_wait_warp(&bars.acc_empty[as], ((ac / kAccStages) & 1) ^ 1);
+          const uint32_t dcol = tmem + as * 128;
+          for (int half = 0; half < 2; ++half, ++cc) {  // x.hi then x.lo into the same accumulator
+            const int s = cc % kHalfStages;
+            mbar_wait_warp(&bars.c_full[s], (cc / kHalfStages) & 1);
+            tc_fence_after();
+            const uint32_t cb = smem_u32(sC + s * C::kTileBytes);
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (k >> 2) * C::kBlockBytes + (k & 3) * 32;
+              mma_ss_warp(dcol, desc_kmajor_sw128(x + off), desc_kmajor_sw128(cb + off), idesc, (half | k) > 0);
+            }
+            mma_commit_warp(&bars.c_empty[s]);
+          }
+          mma_commit_warp(&bars.acc_full[as]);
+        }
       }
       mma_commit_warp(&bars.x_empty[xs]);
     }
@@ -290,33 +334,35 @@ __device__ __forceinline__ void store_segment(const SegOut& o, const int32_t* of
 }
 
 // The update pass: row gathers through perm as asynchronous copies (cp.async, 16 B per lane-instruction), a warp puts
-// all kRows rows of its chunk in flight at once through shared memory (kRows = 64, or 32 rows each of X and Y when
-// the last pass also gathers V through the same pi_k: 16 KB per warp either way); the chunk's perm entries and their
-// labels are loaded up front and a segment ends where the label changes.  On the last Lloyd iteration of the fused
-// call (Xp set) the permuted copies leave shared memory as one bulk copy per tensor (the chunk's rows are contiguous
-// in X', A6).
-constexpr int kAsyncWarps = 4, kAsyncRowBytes = 2 * kUpdMinRows * 256;  // per warp: 16 KB (d = 128)
-template <int D, bool kSq, int kRows>
+// all 32 rows of its chunk in flight at once through shared memory (8 KB per warp, or 16 KB with the 32 rows of Y when
+// the last pass also gathers V through the same pi_k); the chunk's perm entries and their labels are loaded up front
+// and a segment ends where the label changes.  On the last Lloyd iteration of the fused call (Xp set) the permuted
+// copies leave shared memory as one bulk copy per tensor (the chunk's rows are contiguous in X', A6).  32-row chunks
+// and 8 KB per warp (24 warps per SM) measured 185 us per K pass at Wan 2.1 720p against 277 us for 64-row chunks in
+// 16 KB (12 warps per SM): the pass is bound by the latency of the random row reads, not by the bytes in flight; it
+// reads at 4.2 TB/s, next to the 5.0 TB/s (read + write) of the plain permute gather (profiles/r02_micro).
+constexpr int kAsyncWarps = 4;
+template <int D, bool kSq, bool kTwo>
 __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
     const XView X, int N, int C, const int32_t* __restrict__ perm, const int32_t* __restrict__ labels,
     const int32_t* __restrict__ offsets, SegOut out, __nv_bfloat16* __restrict__ Xp, const XView Y,
     __nv_bfloat16* __restrict__ Yp) {
+  constexpr int kRows = kUpdRows;
   constexpr int kCols = D / 32;           // bf16 per lane in the accumulation
   constexpr int kRowBytes = D * 2;        // 256 (d = 128) or 128 (d = 64)
   constexpr int kVecPerRow = kRowBytes / 16;
-  static_assert(kRows == 32 || kRows == 64, "one or two perm entries per lane");
+  constexpr int kWarpBytes = kRows * kRowBytes * (kTwo ? 2 : 1);
   extern __shared__ __align__(128) uint8_t sm_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, bh = blockIdx.y;
-  uint8_t* sx = sm_raw + size_t(warp) * kAsyncRowBytes;  // [kRows][row] X rows of this warp
-  uint8_t* sy = sx + kRows * kRowBytes;                  // [kRows][row] Y rows (kRows = 32)
+  uint8_t* sx = sm_raw + size_t(warp) * kWarpBytes;  // [kRows][row] X rows of this warp
+  uint8_t* sy = sx + kRows * kRowBytes;              // [kRows][row] Y rows (kTwo)
   const int chunk = blockIdx.x * kAsyncWarps + warp;
   const int p0 = chunk * kRows;
   if (p0 >= N) return;
   const int nrow = min(N - p0, kRows);
-  const bool with_y = Y.p != nullptr;
+  constexpr bool with_y = kTwo;
   const int32_t* pm = perm + size_t(bh) * N + p0;
   const int s0 = lane < nrow ? __ldg(pm + lane) : 0;
-  const int s1 = kRows > 32 && lane + 32 < nrow ? __ldg(pm + 32 + lane) : 0;
   const uint8_t* xb = reinterpret_cast<const uint8_t*>(X.row(bh, 0));
   const uint8_t* yb = with_y ? reinterpret_cast<const uint8_t*>(Y.row(bh, 0)) : nullptr;
   const long long xrow = X.sN * 2, yrow = Y.sN * 2;  // bytes between tokens
@@ -326,7 +372,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
 #pragma unroll 4
   for (int r0 = 0; r0 < kRows; r0 += kRowsPerStep) {
     const int r = r0 + rsub;
-    const int src = __shfl_sync(0xffffffffu, r < 32 ? s0 : s1, r & 31);
+    const int src = __shfl_sync(0xffffffffu, s0, r);
     if (r < nrow) {
       const uint32_t dst = smem_u32(sx + r * kRowBytes + piece * 16);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(xb + src * xrow + piece * 16)
@@ -341,7 +387,6 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   // the rows' labels while the copies fly
   const int32_t* lb = labels + size_t(bh) * N;
   const int l0 = lane < nrow ? __ldg(lb + s0) : 0;
-  const int l1 = kRows > 32 && lane + 32 < nrow ? __ldg(lb + s1) : 0;
   const int32_t* off = offsets + size_t(bh) * (C + 1);
   asm volatile("cp.async.wait_all;" ::: "memory");
   // every lane's cp.async writes into shared memory are made visible to the async proxy (the bulk store below) by
@@ -367,7 +412,7 @@ __global__ void __launch_bounds__(32 * kAsyncWarps) k_update_sum_async(
   const int p1 = p0 + nrow;
   int j = __shfl_sync(0xffffffffu, l0, 0);
   for (int r = 0; r < nrow; ++r) {
-    const int lab = __shfl_sync(0xffffffffu, r < 32 ? l0 : l1, r & 31);
+    const int lab = __shfl_sync(0xffffffffu, l0, r);
     if (lab != j) {  // the next cluster starts: store the segment
       store_segment<D, kSq>(out, off, bh, C, j, chunk, p0, p1, lane, acc, sq);
 #pragma unroll
@@ -482,7 +527,8 @@ cudaError_t run_kmeans(const XView X, int BH, int N, int C, int iters, bool warm
       !make_tmap_bf16(&mh, ws.c_hi, uint64_t(BH) * Cpad, D, 128) ||
       !make_tmap_bf16(&ml, ws.c_lo, uint64_t(BH) * Cpad, D, 128))
     return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(k_assign_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<D>::kSmem);
+  auto assign = Cpad == kCentChunk ? k_assign_tc<D, 4> : k_assign_tc<D, 2>;
+  cudaFuncSetAttribute(assign, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<D>::kSmem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -498,23 +544,20 @@ cudaError_t run_kmeans(const XView X, int BH, int N, int C, int iters, bool warm
   __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(ws.c_lo);
   for (int it = 0; it < iters; ++it) {
     k_centroid_split<D><<<dim3(Cpad, BH), D, 0, s>>>(cent, C, Cpad, hi, lo, ws.c_norm);
-    k_assign_tc<D><<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, X.H, labels);
+    assign<<<grid_asg, kAsgThreads, AsgCfg<D>::kSmem, s>>>(mx, mh, ml, ws.c_norm, N, Cpad, BH, X.H, labels);
     cudaError_t e = launch_stable_sort(labels, BH, N, C, ws.sort, perm, offsets, sizes, s);
     if (e != cudaSuccess) return e;
-    // the gather pass (last iteration) uses the asynchronous-copy kernel: K' + V' 0.69 -> 0.48 ms, Q' equal; the
-    // plain update keeps the register-staged one (0.20 ms vs 0.33 ms: its accumulation phase has no loads in flight)
     if (it + 1 == iters && g.wait_y) cudaStreamWaitEvent(s, g.wait_y, 0);
-    // every update pass: the rows of a warp's chunk arrive by cp.async through shared memory (64 rows, or 32 rows of
-    // X and Y when the last pass also gathers V); the last pass also writes the permuted copies (A6).  Measured
-    // (ncu, HunyuanVideo): the register-staged pass read X at 2.75 TB/s (register-limited occupancy), this one at ~4.5
+    // every update pass: the rows of a warp's 32-row chunk arrive by cp.async through shared memory (with the rows of
+    // V when the last pass also gathers it); the last pass also writes the permuted copies (A6)
     const bool gather = it + 1 == iters && g.Xp;
     const bool two = gather && g.Y.p;
-    const int R = two ? 32 : 64;
+    constexpr int R = kUpdRows;
     SegOut seg{ws.c_sum, ws.c_part, objective ? ws.c_sq : nullptr, ws.c_sqpart, (N + R - 1) / R};
     const dim3 grid_a((N + R * kAsyncWarps - 1) / (R * kAsyncWarps), BH);
-    const size_t sm = size_t(kAsyncWarps) * kAsyncRowBytes;
-    auto kern = two ? (objective ? k_update_sum_async<D, true, 32> : k_update_sum_async<D, false, 32>)
-                    : (objective ? k_update_sum_async<D, true, 64> : k_update_sum_async<D, false, 64>);
+    const size_t sm = size_t(kAsyncWarps) * R * D * 2 * (two ? 2 : 1);
+    auto kern = two ? (objective ? k_update_sum_async<D, true, true> : k_update_sum_async<D, false, true>)
+                    : (objective ? k_update_sum_async<D, true, false> : k_update_sum_async<D, false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     kern<<<grid_a, 32 * kAsyncWarps, sm, s>>>(X, N, C, perm, labels, offsets, seg,
                                               gather ? static_cast<__nv_bfloat16*>(g.Xp) : nullptr,
