@@ -156,7 +156,10 @@ SVG2_API svg2_status_t svg2_select_topp(const float* q_centroids, const float* k
  * renormalised over that set (R12), times the matching rows of Vp.  bf16 in, fp32 accumulation (tcgen05/TMEM),
  * bf16 out.  If q_perm is non-NULL the output row is scattered to original order, O[q_perm[p]] (the inverse
  * permutation pi_q^T of PAPER.md:277 fused into the epilogue); otherwise O is written in permuted order.
- * lse [B,H,Nq] f32 (natural log-sum-exp of the scaled scores, same row order as O), nullable. */
+ * lse [B,H,Nq] f32 (natural log-sum-exp of the scaled scores, same row order as O), nullable.
+ * Precondition: every non-empty query cluster selects at least one non-empty key cluster (the fused call guarantees
+ * it, R11).  A cluster that violates it gets no attention work: its O rows are filled with bf16 NaN and its lse
+ * entries with NaN, so the violation is visible (the call still returns SVG2_OK: the mask is device data). */
 SVG2_API svg2_status_t svg2_varblock_attention(const void* Qp, const void* Kp, const void* Vp, svg2_dims_t dims,
                                       const int32_t* q_offsets, const int32_t* k_offsets, const uint8_t* mask,
                                       int32_t Cq, int32_t Ck, float scale, const int32_t* q_perm, void* O,

@@ -116,7 +116,7 @@ def test_kmeans_objective(svg2, oracle_mod, N, d, C, iters):
     Q, K = to_dev(q), to_dev(k)
     _, _, ex = svg2.sparse_attention(Q, K, K, C, C, iters, 0.9, debug=True)
     torch.cuda.synchronize()
-    # the fused call's last update is the gather pass (32-row chunks, not 64): same J up to fp64 rounding order
+    # the fused call's last update is the gather pass (same 32-row chunks as the plain pass): same J
     torch.testing.assert_close(ex["q_objective"], obj, rtol=1e-12, atol=0)
     _, _, _, kobj = svg2.kmeans(K, C, iters, return_objective=True)
     torch.testing.assert_close(ex["k_objective"], kobj, rtol=1e-12, atol=0)
@@ -318,6 +318,36 @@ def test_varblock_lse(svg2, oracle_mod):
                                            lq=lq.cpu().numpy()[0, 0], lk=lk.cpu().numpy()[0, 0],
                                            mask=mask.cpu().numpy()[0, 0], return_lse=True)
     assert np.max(np.abs(lse.cpu().numpy()[0, 0] - ref_lse)) < 1e-2
+
+
+def test_varblock_empty_selection_rows_are_nan(svg2, oracle_mod):
+    """The svg2_varblock_attention precondition (include/svg2.h): a query cluster whose mask row selects no non-empty
+    key cluster gets NaN output rows and NaN lse (never unwritten memory); every other row is unaffected (bitwise)."""
+    Q, K, V, Cq, Ck, p, iters = _pipeline_inputs(svg2, (1, 2, 2000, 2000, 128, 12, 24), seed=6)
+    lq, sq, cq, pq, oq = svg2.kmeans(Q, Cq, iters, return_perm=True)
+    lk, sk, ck, pk, ok = svg2.kmeans(K, Ck, iters, return_perm=True)
+    _, _, Qp, _ = svg2.permute(lq, Cq, Q)
+    _, _, Kp, Vp = svg2.permute(lk, Ck, K, V)
+    mask, _ = svg2.select_topp(cq, ck, sq, sk, p)
+    O, lse = svg2.varblock_attention(Qp, Kp, Vp, oq, ok, mask, q_perm=pq, return_lse=True)
+    bad = mask.clone()
+    sq_h = sq.cpu().numpy()
+    i0 = int(np.argmax(sq_h[0, 1]))  # the largest query cluster of head 1: select nothing
+    bad[0, 1, i0] = 0
+    # and a row of head 0 that selects only empty key clusters (if any exist), else nothing at all
+    empty_k = np.flatnonzero(sk.cpu().numpy()[0, 0] == 0)
+    i1 = int(np.argmax(sq_h[0, 0]))
+    bad[0, 0, i1] = 0
+    if empty_k.size:
+        bad[0, 0, i1, torch.as_tensor(empty_k, device=bad.device)] = 1
+    O2, lse2 = svg2.varblock_attention(Qp, Kp, Vp, oq, ok, bad, q_perm=pq, return_lse=True)
+    lq_h = lq.cpu().numpy()
+    for h, i in ((0, i1), (1, i0)):
+        rows = torch.as_tensor(np.flatnonzero(lq_h[0, h] == i), device=O.device)
+        assert rows.numel() == sq_h[0, h, i] > 0
+        assert torch.isnan(O2[0, h, rows].float()).all() and torch.isnan(lse2[0, h, rows]).all()
+        keep = torch.as_tensor(np.flatnonzero(lq_h[0, h] != i), device=O.device)
+        assert torch.equal(O2[0, h, keep], O[0, h, keep]) and torch.equal(lse2[0, h, keep], lse[0, h, keep])
 
 
 # ------------------------------------------------------------------ P6: fused call, stage by stage
