@@ -139,7 +139,7 @@ __device__ long long g_trace[kTrEv][kTrT];
 // power-of-two boxes covering it.  The stage's mbarrier receives ngt x 8 rows x D x 2 bytes.
 template <int D>
 __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* stage, uint64_t* bar, int ngt, int lane,
-                                             int2 gw) {
+                                             int2 gw, uint64_t policy) {
   using C = Cfg<D>;
   const int prev_row = __shfl_up_sync(0xffffffffu, gw.x, 1);
   const int prev_nv = __shfl_up_sync(0xffffffffu, gw.y, 1);
@@ -156,7 +156,7 @@ __device__ __forceinline__ void load_kv_tile(const CUtensorMap* maps, uint8_t* s
       const int pw = 1 << kind;
 #pragma unroll
       for (int b = 0; b < C::kBlocks; ++b)
-        tma_load_2d(stage + b * C::kKBlockBytes + pos * 1024, &maps[kind], bar, 64 * b, row);
+        tma_load_2d_hint(stage + b * C::kKBlockBytes + pos * 1024, &maps[kind], bar, 64 * b, row, policy);
       pos += pw;
       len -= pw;
       row += 8 * pw;
@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint64_t* full = vrole ? bars.v_full : bars.k_full;
       uint64_t* empty = vrole ? bars.v_empty : bars.k_empty;
       uint32_t qph = 0, ks = 0, kph = 0, islot = 0, iph = 0;
+      // L2 policies: K' / V' rows are re-read by every query cluster of the head that selects them (keep them),
+      // Q' rows are read once (let them go first)
+      const uint64_t pol_kv = l2_policy_evict_last(), pol_q = l2_policy_evict_first();
       bool tr_first = true;
       (void)tr_first;
       while (true) {
@@ -268,9 +271,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             mbar_arrive_expect_tx(&bars.q_full, (nb > 0 ? 2u : 1u) * C::kQTileBytes);
             for (int b = 0; b < C::kBlocks; ++b) {
-              tma_load_2d(sQ + b * C::kQBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x);
+              tma_load_2d_hint(sQ + b * C::kQBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x, pol_q);
               if (nb > 0)
-                tma_load_2d(sQ + C::kQTileBytes + b * C::kQBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x + 128);
+                tma_load_2d_hint(sQ + C::kQTileBytes + b * C::kQBlockBytes, &mapQ, &bars.q_full, 64 * b, it.x + 128,
+                                 pol_q);
             }
           }
           qph ^= 1;
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[ks], kph ^ 1);
           if (lane == 0) mbar_arrive_expect_tx(&full[ks], uint32_t(ngt) * C::kGroupBytes);
           __syncwarp();
-          load_kv_tile<D>(maps, ring + ks * C::kKTileBytes, &full[ks], ngt, lane, gw);
+          load_kv_tile<D>(maps, ring + ks * C::kKTileBytes, &full[ks], ngt, lane, gw, pol_kv);
           TRACE(vrole ? 1 : 0, t);
           gw = gw_next;
           if (++ks == kSt) {
@@ -594,8 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e)
                 r[e] = __uint_as_float(oa[8 * v + e]) * ca + __uint_as_float(ob[8 * v + e]) * cb;
-              orow[4 * c + v] = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
-                                           pack_bf16x2(r[6], r[7]));
+              __stcs(orow + 4 * c + v, make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]),
+                                                  pack_bf16x2(r[4], r[5]), pack_bf16x2(r[6], r[7])));
             }
           }
         }
@@ -631,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             u.y = pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l);
             u.z = pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l);
             u.w = pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l);
-            orow[4 * c + v] = u;
+            __stcs(orow + 4 * c + v, u);  // streamed: O is not re-read by this kernel
           }
         }
       }
