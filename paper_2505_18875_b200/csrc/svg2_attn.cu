@@ -684,23 +684,22 @@ cudaError_t run_attn(const void* Qp, const void* Kp, const void* Vp, int BH, int
 }
 
 // ---------------------------------------------------------------- work-list builder
-constexpr int kBuildThreads = 128;
-
-// block-wide exclusive scan (kBuildThreads threads, one value each); *total receives the block sum
-__device__ int build_scan(int v, int* total) {
-  __shared__ int wsum[kBuildThreads / 32];
+// block-wide exclusive scan (NT threads, one value each); *total receives the block sum
+template <int NT, typename T>
+__device__ T build_scan(T v, T* total) {
+  __shared__ T wsum[NT / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = v;
+  T x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) wsum[w] = x;
   __syncthreads();
-  int before = 0, tot = 0;
+  T before = 0, tot = 0;
 #pragma unroll
-  for (int k = 0; k < kBuildThreads / 32; ++k) {
+  for (int k = 0; k < NT / 32; ++k) {
     before += k < w ? wsum[k] : 0;
     tot += wsum[k];
   }
@@ -711,9 +710,11 @@ __device__ int build_scan(int v, int* total) {
 
 // One CTA per (b,h,i): the key stream of query cluster i = its selected, non-empty key clusters in ascending j,
 // contiguous clusters merged into runs, runs cut into 8-row groups (the last one partial), the stream padded to an
-// even group count; plus the packed 4-bit valid counts per gpt-group tile.  Three block scans (selected clusters,
-// run starts, groups per run) make every step parallel.
-__global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* __restrict__ k_off,
+// even group count; plus the packed 4-bit valid counts per gpt-group tile.  Three block scans (selected clusters with
+// their key rows packed into one 64-bit scan, run starts, groups per run) make every step parallel; NT = 512 threads
+// for C_k > 1024 so a mask row takes few scan rounds.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_build_streams(const int32_t* __restrict__ k_off,
                                                                  const uint8_t* __restrict__ mask, int Nk, int Cq,
                                                                  int Ck, int gpt, AttnWs ws) {
   extern __shared__ int sbuf[];
@@ -727,8 +728,9 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   const uint8_t* mrow = mask + li * Ck;
   const int32_t* ko = k_off + size_t(bh) * (Ck + 1);
   // 1) compact the selected, non-empty clusters (ascending j); count the stream's key rows
-  int base = 0, nkeys = 0;
-  for (int j0 = 0; j0 < Ck; j0 += kBuildThreads) {
+  int base = 0;
+  long long nkeys = 0;
+  for (int j0 = 0; j0 < Ck; j0 += NT) {
     const int j = j0 + tid;
     int s = 0, e = 0, f = 0;
     if (j < Ck && mrow[j]) {
@@ -736,32 +738,31 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
       e = __ldg(ko + j + 1);
       f = e > s;
     }
-    int tot, rows;
-    const int pos = base + build_scan(f, &tot);
+    long long tot;  // (key rows << 20) | selected clusters: one scan for both (<= NT clusters per round)
+    const int pos = base + int(build_scan<NT, long long>((static_cast<long long>(e - s) << 20) | f, &tot) & 0xFFFFF);
     if (f) {
       sel_s[pos] = s;
       sel_e[pos] = e;
     }
-    base += tot;
-    build_scan(e - s, &rows);
-    nkeys += rows;
+    base += int(tot & 0xFFFFF);
+    nkeys += tot >> 20;
   }
-  if (tid == 0) ws.keys[li] = nkeys;
+  if (tid == 0) ws.keys[li] = int(nkeys);
   const int nsel = base;
   __syncthreads();
   // 2) runs: a selected cluster starts a run unless it begins exactly where the previous one ends
   base = 0;
-  for (int k0 = 0; k0 < nsel; k0 += kBuildThreads) {
+  for (int k0 = 0; k0 < nsel; k0 += NT) {
     const int k = k0 + tid;
     const int f = (k < nsel) && (k == 0 || sel_s[k] != sel_e[k - 1]);
     int tot;
-    const int r = base + build_scan(f, &tot);
+    const int r = base + build_scan<NT, int>(f, &tot);
     if (f) run_s[r] = sel_s[k];
     base += tot;
   }
   const int nrun = base;
   __syncthreads();
-  for (int k = tid; k < nsel; k += kBuildThreads) {  // the last cluster of each run writes the run end
+  for (int k = tid; k < nsel; k += NT) {  // the last cluster of each run writes the run end
     const bool last = (k == nsel - 1) || (sel_s[k + 1] != sel_e[k]);
     if (last) {
       int lo = 0, hi = nrun - 1;  // the run containing cluster k: last run start <= its start
@@ -775,11 +776,11 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   __syncthreads();
   // 3) groups per run -> group offsets
   base = 0;
-  for (int r0 = 0; r0 < nrun; r0 += kBuildThreads) {
+  for (int r0 = 0; r0 < nrun; r0 += NT) {
     const int r = r0 + tid;
     const int gr = r < nrun ? (run_e[r] - run_s[r] + 7) / 8 : 0;
     int tot;
-    const int g0 = base + build_scan(gr, &tot);
+    const int g0 = base + build_scan<NT, int>(gr, &tot);
     if (r < nrun) run_g[r] = g0;
     base += tot;
   }
@@ -796,7 +797,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_streams(const int32_t* 
   // writing the group words and packing the tile's 4-bit valid counts in the same pass
   uint64_t* tw = ws.tilew + li * ws.tcap;
   const int ntiles = (ng + gpt - 1) / gpt;
-  for (int t = tid; t < ntiles; t += kBuildThreads) {
+  for (int t = tid; t < ntiles; t += NT) {
     const int g0 = t * gpt, g1 = min(ng, g0 + gpt);
     int r = 0;
     if (g0 < ng_real) {
@@ -961,8 +962,13 @@ cudaError_t launch_build_worklist(const int32_t* q_offsets, const int32_t* k_off
                                   int Nq, int Nk, int Cq, int Ck, int gpt, AttnWs ws, OrphanFill of, cudaStream_t s,
                                   QPart part) {
   const size_t smem = (5 * size_t(Ck) + 1) * sizeof(int);
-  cudaFuncSetAttribute(k_build_streams, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  k_build_streams<<<dim3(Cq, BH), kBuildThreads, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, gpt, ws);
+  if (Ck > 1024) {
+    cudaFuncSetAttribute(k_build_streams<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_build_streams<512><<<dim3(Cq, BH), 512, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, gpt, ws);
+  } else {
+    cudaFuncSetAttribute(k_build_streams<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_build_streams<128><<<dim3(Cq, BH), 128, smem, s>>>(k_offsets, mask, Nk, Cq, Ck, gpt, ws);
+  }
   k_parts<<<BH, 1024, 0, s>>>(q_offsets, Cq, part, ws);
   k_items<<<1, 1024, 0, s>>>(q_offsets, BH, Nq, Cq, gpt, ws, of);
   return cudaGetLastError();
