@@ -245,6 +245,60 @@ def test_select_topp_bitexact(svg2, oracle_mod, p, Cq, Ck, d):
             assert pairs_h[0, h] == opairs
 
 
+@pytest.mark.parametrize("p", [0.5, 0.9])
+@pytest.mark.parametrize("Cq,Ck", [(9, 300), (9, 1500), (5, 4000)])
+def test_select_topp_diffuse_weights(svg2, oracle_mod, p, Cq, Ck):
+    """Near-uniform Eq. 2 weights (centroids almost equal, sizes 5..9): every w of a row shares one or two binades, so
+    the threshold search narrows long lists (svg2_select.cu) instead of resolving a short one.  Masks as in
+    test_select_topp_bitexact: equal to the oracle's except R17 near-ties."""
+    rng = np.random.default_rng(Cq + Ck)
+    B, H, d = 1, 2, 128
+    cq = (rng.standard_normal((B, H, Cq, d)) * 0.05).astype(np.float32)
+    ck = (rng.standard_normal((B, H, Ck, d)) * 0.05).astype(np.float32)
+    sq = rng.integers(1, 50, (B, H, Cq)).astype(np.int32)
+    sk = rng.integers(5, 10, (B, H, Ck)).astype(np.int32)
+    mask, pairs = svg2.select_topp(*(torch.from_numpy(a).cuda() for a in (cq, ck, sq, sk)), p)
+    mask_h, pairs_h = mask.cpu().numpy(), pairs.cpu().numpy()
+    for h in range(H):
+        om, opairs, S, W, Z = oracle_mod.select_topp(cq[0, h].astype(np.float64), ck[0, h].astype(np.float64),
+                                                     sq[0, h], sk[0, h], d, f32scale(d), p, return_tables=True)
+        assert W[:, :].max() < 4 * W[:, :].min()  # the construction: one or two binades per row
+        nrows, nontie = mask_mismatch_rows_are_ties(W, Z, sk[0, h], p, mask_h[0, h], om)
+        assert nontie == 0
+        if nrows == 0:
+            assert pairs_h[0, h] == opairs
+
+
+@pytest.mark.parametrize("Ck", [64, 700, 1500, 3000])
+def test_select_topp_exact_ties_follow_j(svg2, oracle_mod, Ck):
+    """Equal weights at the top-p boundary (key clusters in groups of 4 with identical centroids and sizes): the sorted
+    walk of R11 takes the tied clusters in ascending j, and p is placed half-way through a tie group (far from any
+    R17 near-tie of the cumulative mass), so the GPU's threshold selection must equal the oracle's mask exactly."""
+    rng = np.random.default_rng(Ck)
+    d = 128
+    groups = Ck // 4
+    ck = np.repeat((rng.standard_normal((groups, d)) * 0.3).astype(np.float32), 4, axis=0)
+    sk = np.repeat(rng.integers(1, 40, groups), 4).astype(np.int32)
+    perm = rng.permutation(Ck)  # spread each tie group over non-adjacent j
+    ck, sk = ck[perm], sk[perm]
+    cq = (rng.standard_normal((1, d)) * 0.3).astype(np.float32)
+    sq = np.array([17], np.int32)
+    _, _, S, W, Z = oracle_mod.select_topp(cq.astype(np.float64), ck.astype(np.float64), sq, sk, d, f32scale(d), 0.5,
+                                           return_tables=True)
+    order = sorted(range(Ck), key=lambda j: (-W[0, j], j))
+    w = W[0, order]
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    g0 = int(np.searchsorted(cum, 0.6 * Z[0]))
+    g0 -= g0 % 4  # the first rank of a tie group (ranks of a group are consecutive: equal w)
+    assert np.all(w[g0:g0 + 4] == w[g0])
+    p = (cum[g0] + 1.5 * w[g0]) / Z[0]
+    om, opairs = oracle_mod.select_topp(cq.astype(np.float64), ck.astype(np.float64), sq, sk, d, f32scale(d), p)
+    mask, pairs = svg2.select_topp(*(torch.from_numpy(a[None, None]).cuda() for a in (cq, ck, sq, sk)), p)
+    assert int(om.sum()) == g0 + 2
+    assert np.array_equal(mask.cpu().numpy()[0, 0], om)
+    assert int(pairs.cpu().numpy()[0, 0]) == opairs
+
+
 # ------------------------------------------------------------------ P5: variable-block attention
 def _pipeline_inputs(svg2, wl_or_shape, seed=0, top_p=None, iters=None, dup=False, amp=None):
     if isinstance(wl_or_shape, svg2_synth.Workload):
