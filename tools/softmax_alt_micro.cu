@@ -19,13 +19,23 @@ __device__ __forceinline__ uint32_t (&sub16(uint32_t (&a)[N], int off))[16] { re
 template <int N>
 __device__ __forceinline__ uint32_t (&sub8(uint32_t (&a)[N], int off))[8] { return *reinterpret_cast<uint32_t(*)[8]>(a + off); }
 constexpr int kN = 80, kIters = 256;
+#define R4(i) "=r"(r[i]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3])
+__device__ __forceinline__ void ld_x8(uint32_t t, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : R4(0), R4(4) : "r"(t));
+}
+__device__ __forceinline__ void ld_x4(uint32_t t, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];" : R4(0) : "r"(t));
+}
+template <int N>
+__device__ __forceinline__ uint32_t (&sub4(uint32_t (&a)[N], int off))[4] { return *reinterpret_cast<uint32_t(*)[4]>(a + off); }
 
 // kMode bits: 1 = S from TMEM, 2 = exponential turns, 4 = P stored to TMEM, 8 = launder S through FADDs before the
 // barrier, 16 = warpgroup b idles (one softmax warp per SMSP)
 template <int kMode, int kPoly = 0>
 __global__ void __launch_bounds__(256, 1) k(uint32_t* out, long long* cyc) {
   constexpr bool kTmem = kMode & 1, kTurns = kMode & 2, kStore = kMode & 4, kLaunder = kMode & 8, kSolo = kMode & 16;
-  constexpr bool kLdInTurn = kMode & 32;  // the S load waits for the turn (its address depends on a load after it)
+  constexpr bool kLdInTurn = kMode & 32;
+  constexpr bool kLd8 = kMode & 64, kLd4 = kMode & 128;  // S loaded as 10 x8 / 20 x4 loads instead of x32, x32, x16  // the S load waits for the turn (its address depends on a load after it)
   __shared__ uint32_t tmem_slot;
   __shared__ float zero_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = warp >> 2;
@@ -70,9 +80,17 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, long long* cyc) {
 #pragma unroll
       for (int e = 0; e < kN; ++e) s[e] = sreg[e] ^ (uint32_t(it) & 1u);
     } else {
-      tmem_ld32(tSx, sub32(s, 0));
-      tmem_ld32(tSx + 32, sub32(s, 32));
-      tmem_ld16(tSx + 64, sub16(s, 64));
+      if (kLd8) {
+#pragma unroll
+        for (int c = 0; c < kN / 8; ++c) ld_x8(tSx + 8 * c, sub8(s, 8 * c));
+      } else if (kLd4) {
+#pragma unroll
+        for (int c = 0; c < kN / 4; ++c) ld_x4(tSx + 4 * c, sub4(s, 4 * c));
+      } else {
+        tmem_ld32(tSx, sub32(s, 0));
+        tmem_ld32(tSx + 32, sub32(s, 32));
+        tmem_ld16(tSx + 64, sub16(s, 64));
+      }
       tmem_wait_ld();
       if (kLaunder) {
 #pragma unroll
@@ -174,6 +192,9 @@ int main() {
   run<1 | 4 | 8 | 16>("TMEM ld+st, laundered, solo");
   run<1 | 2 | 4 | 32>("TMEM ld+st, ld in turn");
   run<1 | 2 | 32>("TMEM ld only, ld in turn");
+  run<1 | 2 | 4 | 64>("TMEM ld(x8)+st, turns");
+  run<1 | 2 | 4 | 128>("TMEM ld(x4)+st, turns");
+  run<1 | 4 | 64>("TMEM ld(x8)+st, no turns");
   run<1 | 2 | 4, 1>("TMEM ld+st, turns, poly 1/8");
   run<1 | 2 | 4, 2>("TMEM ld+st, turns, poly 2/8");
   run<1 | 2 | 4, 3>("TMEM ld+st, turns, poly 3/8");
