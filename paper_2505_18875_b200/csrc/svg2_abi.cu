@@ -18,7 +18,12 @@ constexpr int kHostSlots = 3, kHostComputeStreams = 3;  // e2e HunyuanVideo: 62.
 // 2 / 3 / 4 / 6 middle chunks + ramp, 64.6 ms with 6 equal chunks; two compute streams: 59.7 / 57.5 / 58.4 ms with
 // 4 / 6 / 9)
 constexpr int kHostChunks = 6;
-static_assert(kHostChunks + 4 <= kMaxHostChunks, "host chunks");
+// chunk sizes (heads) before and after the middle chunks: only the first chunk's upload and the last chunk's download
+// are not overlapped with computation
+// (e2e, HunyuanVideo, interleaved A/B on one box: 1,1,2,2 | 6 | 2,1 -> 52.98 ms mean of 4 vs 53.72 for 1,2 | 6 | 2,1;
+// 1,1,2 | 6 | 1 53.8-54.2, 1,2 | 8 | 1 53.4-53.6, 1,1,1,2 | 5 | 1,1 54.0-56.0)
+constexpr int kRampUp[] = {1, 1, 2, 2}, kRampDown[] = {2, 1};
+static_assert(kHostChunks + 16 <= kMaxHostChunks, "host chunks");
 
 svg2_status_t check_device() {
   int dev = 0, major = 0, minor = 0;
@@ -236,20 +241,24 @@ struct HostPlan {
   int start[kMaxHostChunks + 1];  // chunk c = heads [start[c], start[c+1])
 };
 // Head chunks of the host pipeline.  Only the first chunk's upload and the last chunk's download are not overlapped
-// with computation, so the chunks ramp up 1, 2 heads at the start and down 2, 1 at the end around equal middle
-// chunks (kHostChunks of them); small problems get one chunk per head.
+// with computation, so the chunks ramp up (kRampUp: each upload shorter than the computation of the chunks before
+// it) and down (kRampDown) around equal middle chunks (kHostChunks of them); small problems get one chunk per head.
 HostPlan host_plan(const svg2_dims_t& dm) {
   HostPlan p;
   p.BH = dm.B * dm.H;
   int sizes[kMaxHostChunks], n = 0;
   const int mid_chunks = kHostChunks;
   int rest = p.BH;
-  const int ramp[2] = {1, 2};
-  const bool use_ramp = p.BH >= 2 * (ramp[0] + ramp[1]) + mid_chunks;
+  const int* up = kRampUp;
+  const int* down = kRampDown;
+  constexpr int nup = sizeof(kRampUp) / sizeof(int), ndown = sizeof(kRampDown) / sizeof(int);
+  int ramp_heads = 0;
+  for (int i = 0; i < nup; ++i) ramp_heads += up[i];
+  for (int i = 0; i < ndown; ++i) ramp_heads += down[i];
+  const bool use_ramp = p.BH >= ramp_heads + mid_chunks;
   if (use_ramp) {
-    sizes[n++] = ramp[0];
-    sizes[n++] = ramp[1];
-    rest -= 2 * (ramp[0] + ramp[1]);
+    for (int i = 0; i < nup; ++i) sizes[n++] = up[i];
+    rest -= ramp_heads;
   }
   const int m = rest < mid_chunks ? (rest > 0 ? rest : 1) : mid_chunks;
   for (int i = 0; i < m && rest > 0; ++i) {  // equal middle chunks (the first ones one head larger if uneven)
@@ -257,10 +266,8 @@ HostPlan host_plan(const svg2_dims_t& dm) {
     sizes[n++] = sz;
     rest -= sz;
   }
-  if (use_ramp) {
-    sizes[n++] = ramp[1];
-    sizes[n++] = ramp[0];
-  }
+  if (use_ramp)
+    for (int i = 0; i < ndown; ++i) sizes[n++] = down[i];
   p.nchunks = n;
   p.hc = 1;
   p.start[0] = 0;
