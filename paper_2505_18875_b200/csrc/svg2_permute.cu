@@ -170,17 +170,16 @@ __global__ void k_scatter_rows(const uint4* __restrict__ Op, const int32_t* __re
 }
 
 // FP8 PV path: per (b,h) and channel c the largest |x_c| (bf16 -> f32, as float bits: non-negative floats order like
-// uints).  The grid stride is a multiple of the vectors per row, so a thread always reads the same 8 channels.
-__global__ void k_absmax(const XView X, long long vec_per_bh, int vec_per_row, uint32_t* __restrict__ amax) {
-  const int bh = blockIdx.y;
+// uints).  Grid (blocks per head, B*H); 32-bit indices within a head (N * d/8 < 2^31), vec_per_row = 1 << lg; the
+// stride is a multiple of the vectors per row, so a thread always reads the same 8 channels; four loads in flight.
+__global__ void k_absmax(const XView X, int vec_per_bh, int lg, uint32_t* __restrict__ amax) {
+  const int bh = blockIdx.y, vpr = 1 << lg;
   const uint16_t* xb = X.row(bh, 0);
-  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, S = gridDim.x * blockDim.x, v = t0 & (vpr - 1);
   float m[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) m[e] = 0.f;
-  for (long long t = t0; t < vec_per_bh; t += (long long)gridDim.x * blockDim.x) {
-    const long long n = t / vec_per_row;
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(xb + n * X.sN) + (t - n * vec_per_row));
+  auto fold = [&](const uint4& u) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -188,40 +187,66 @@ __global__ void k_absmax(const XView X, long long vec_per_bh, int vec_per_row, u
       m[2 * e] = fmaxf(m[2 * e], fabsf(f.x));
       m[2 * e + 1] = fmaxf(m[2 * e + 1], fabsf(f.y));
     }
+  };
+  auto load = [&](int t) { return __ldg(reinterpret_cast<const uint4*>(xb + (long long)(t >> lg) * X.sN) + v); };
+  int t = t0;
+  for (; t + 3 * S < vec_per_bh; t += 4 * S) {
+    const uint4 u0 = load(t), u1 = load(t + S), u2 = load(t + 2 * S), u3 = load(t + 3 * S);
+    fold(u0);
+    fold(u1);
+    fold(u2);
+    fold(u3);
   }
+  for (; t < vec_per_bh; t += S) fold(load(t));
   // lanes l and l ^ o (o >= vec_per_row) hold the same channels
-  for (int o = 16; o >= vec_per_row; o >>= 1)
+  for (int o = 16; o >= vpr; o >>= 1)
 #pragma unroll
     for (int e = 0; e < 8; ++e) m[e] = fmaxf(m[e], __shfl_xor_sync(0xffffffffu, m[e], o));
-  if ((threadIdx.x & 31) < vec_per_row) {
-    const int c0 = int(t0 % vec_per_row) * 8;
+  if ((threadIdx.x & 31) < vpr) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) atomicMax(amax + size_t(bh) * vec_per_row * 8 + c0 + e, __float_as_uint(m[e]));
+    for (int e = 0; e < 8; ++e) atomicMax(amax + size_t(bh) * vpr * 8 + v * 8 + e, __float_as_uint(m[e]));
   }
 }
 
 // FP8 PV path: V' = V[perm] rounded to e4m3, channel c scaled by 448 / amax_c of its head (448 = largest finite e4m3);
-// the attention epilogue multiplies output channel c by amax_c / 448
-__global__ void k_gather_rows_e4m3(const int32_t* __restrict__ perm, long long rows, int N, int vec_per_row,
-                                   const XView X, uint2* __restrict__ Xq, const uint32_t* __restrict__ amax) {
-  const long long total = rows * vec_per_row;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long r = t / vec_per_row;
-    const int v = int(t - r * vec_per_row);
-    const int bh = int(r / N);
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(X.row(bh, __ldg(perm + r))) + v);
+// the attention epilogue multiplies output channel c by amax_c / 448.  Same grid as k_absmax: a thread keeps its head
+// and its 8 channels, so the scales are computed once; four rows in flight per thread.
+__global__ void k_gather_rows_e4m3(const int32_t* __restrict__ perm, int N, int lg, const XView X,
+                                   uint2* __restrict__ Xq, const uint32_t* __restrict__ amax) {
+  const int bh = blockIdx.y, vpr = 1 << lg, total = N << lg;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, S = gridDim.x * blockDim.x, v = t0 & (vpr - 1);
+  float sc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float a = __uint_as_float(__ldg(amax + (size_t(bh) * vpr + v) * 8 + e));
+    sc[e] = a > 0.f ? 448.f / a : 1.f;
+  }
+  const int32_t* pb = perm + size_t(bh) * N;
+  uint2* qb = Xq + size_t(bh) * total;
+  auto quant = [&](int t, const uint4& u) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-    const uint32_t* am = amax + ((long long)bh * vec_per_row + v) * 8;
     uint32_t q[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float a0 = __uint_as_float(__ldg(am + 2 * e)), a1 = __uint_as_float(__ldg(am + 2 * e + 1));
       const float2 f = __bfloat1622float2(h[e]);
-      q[e] = pack_e4m3x2(f.x * (a0 > 0.f ? 448.f / a0 : 1.f), f.y * (a1 > 0.f ? 448.f / a1 : 1.f));
+      q[e] = pack_e4m3x2(f.x * sc[2 * e], f.y * sc[2 * e + 1]);
     }
-    Xq[r * vec_per_row + v] = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
+    qb[t] = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
+  };
+  auto src = [&](int t) { return reinterpret_cast<const uint4*>(X.row(bh, __ldg(pb + (t >> lg)))) + v; };
+  int t = t0;
+  for (; t + 3 * S < total; t += 4 * S) {
+    const uint4* p0 = src(t);
+    const uint4* p1 = src(t + S);
+    const uint4* p2 = src(t + 2 * S);
+    const uint4* p3 = src(t + 3 * S);
+    const uint4 u0 = __ldg(p0), u1 = __ldg(p1), u2 = __ldg(p2), u3 = __ldg(p3);
+    quant(t, u0);
+    quant(t + S, u1);
+    quant(t + 2 * S, u2);
+    quant(t + 3 * S, u3);
   }
+  for (; t < total; t += S) quant(t, __ldg(src(t)));
 }
 
 int copy_grid(long long work) {
@@ -257,15 +282,15 @@ cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const 
 
 cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq, uint32_t* amax,
                                     cudaStream_t s) {
-  const long long rows = (long long)BH * N;
   const int vpr = d / 8;
   cudaMemsetAsync(amax, 0, size_t(BH) * d * sizeof(uint32_t), s);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int per_bh = (sms * 8 + BH - 1) / BH;
-  k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(X, (long long)N * vpr, vpr, amax);
-  k_gather_rows_e4m3<<<copy_grid(rows * vpr), 256, 0, s>>>(perm, rows, N, vpr, X, static_cast<uint2*>(Xq), amax);
+  const int lg = 31 - __builtin_clz(unsigned(vpr));  // d / 8 = 8 or 16
+  k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(X, N * vpr, lg, amax);
+  k_gather_rows_e4m3<<<dim3(per_bh, BH), 256, 0, s>>>(perm, N, lg, X, static_cast<uint2*>(Xq), amax);
   return cudaGetLastError();
 }
 
