@@ -146,8 +146,7 @@ struct AttnWs {
   int2* groups;        // [BH, Cq, group_cap]
   uint64_t* tilew;     // [BH, Cq, tile_cap]
   int32_t* ngroups;    // [BH, Cq]
-  int4* items_bh;      // [BH, cap]
-  int32_t* items_cnt;  // [BH]
+  int32_t* order;      // [BH, Cq] query clusters of each head in work-list order (longest key stream first)
   int4* items;         // [BH * cap] flattened
   int32_t* n_items;    // [3]: item count, dynamic-scheduler counter, query rows with an empty key stream
   long long* keys;     // [BH, Cq] selected key rows of each query cluster's stream
@@ -162,8 +161,7 @@ inline AttnWs carve_attn(Carver& c, int BH, int Nq, int Nk, int Cq, int Ck) {
   w.groups = c.take<int2>(size_t(BH) * Cq * w.gcap);
   w.tilew = c.take<uint64_t>(size_t(BH) * Cq * w.tcap);
   w.ngroups = c.take<int32_t>(size_t(BH) * Cq);
-  w.items_bh = c.take<int4>(size_t(BH) * cap);
-  w.items_cnt = c.take<int32_t>(BH);
+  w.order = c.take<int32_t>(size_t(BH) * Cq);
   w.items = c.take<int4>(size_t(BH) * cap);
   w.n_items = c.take<int32_t>(3);
   w.keys = c.take<long long>(size_t(BH) * Cq);

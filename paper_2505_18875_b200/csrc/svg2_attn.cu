@@ -868,8 +868,9 @@ __global__ void __launch_bounds__(1024) k_parts(const int32_t* __restrict__ q_of
   }
 }
 
-// Work items in (b,h)-major, cluster order: ceil(|Q_i| / 256) pairs of 128-row Q tiles per non-empty query cluster
-// with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.  A
+constexpr int kOrderMaxCq = 512;
+// Work items in (b,h)-major order, clusters of a head longest key stream first: ceil(|Q_i| / 256) pairs of 128-row Q
+// tiles per non-empty query cluster with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.  A
 // query cluster whose mask row selects no non-empty key cluster (a contract violation of svg2_varblock_attention,
 // include/svg2.h; impossible in the fused call, where every row selects >= 1 non-empty cluster) gets no item: its
 // output rows (and lse) are filled with NaN here, so the violation is visible instead of leaving memory unwritten,
@@ -880,14 +881,32 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
   __shared__ int n_orphan;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) n_orphan = 0;
-  __syncthreads();
   const int total_clusters = BH * Cq;
+  // Within each head the clusters are listed longest key stream first (ties: lower index), so the launch ends on
+  // short items and the persistent CTAs finish together; heads stay in order (their K'/V' stay in L2 one head at a
+  // time).  O(Cq^2) per head: only for Cq <= kOrderMaxCq, else index order.
+  for (int c = tid; c < total_clusters; c += 1024) {
+    const int bh = c / Cq, i = c - bh * Cq;
+    int rank = i;
+    if (Cq <= kOrderMaxCq) {
+      const int32_t* ng = ws.ngroups + size_t(bh) * Cq;
+      const int gi = ng[i];
+      rank = 0;
+      for (int k = 0; k < Cq; ++k) {
+        const int gk = ng[k];
+        rank += (gk > gi || (gk == gi && k < i)) ? 1 : 0;
+      }
+    }
+    ws.order[size_t(bh) * Cq + rank] = i;
+  }
+  __syncthreads();
   int base = 0;
   for (int c0 = 0; c0 < total_clusters; c0 += 1024) {
-    const int c = c0 + tid;
+    int c = c0 + tid;
     int n = 0, q0 = 0, sq = 0, bh = 0;
     if (c < total_clusters) {
       bh = c / Cq;
+      c = bh * Cq + ws.order[c];  // the cluster at this position of the head's order
       const int i = c - bh * Cq;
       q0 = q_off[size_t(bh) * (Cq + 1) + i];
       sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q0;
