@@ -121,6 +121,11 @@ struct Params {
 
 // Measurement build only (-DSVG2_TRACE, tools/trace_attn.py): clock64 per event and key tile of the first item of
 // CTA 0, printed at kernel exit.  The product build compiles no trace code.
+#ifdef SVG2_CTA_TIMES
+// measurement build only (-DSVG2_CTA_TIMES, tools/cta_times.py): per CTA the globaltimer at start and exit and the
+// number of items it processed
+__device__ unsigned long long g_cta_times[1024][3];
+#endif
 #ifdef SVG2_TRACE
 constexpr int kTrT = 48, kTrEv = 24;
 __device__ long long g_trace[kTrEv][kTrT];
@@ -222,6 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
   const int n_items = __ldg(p.n_items);
+#ifdef SVG2_CTA_TIMES
+  if (threadIdx.x == 0) {
+    g_cta_times[blockIdx.x][0] = globaltimer_ns();
+    g_cta_times[blockIdx.x][2] = 0;
+  }
+#endif
 
   if (warp >= 8) {
     reg_dealloc<kRegsCtl>();
@@ -246,6 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           int item = 0;
           if (lane == 0) item = atomicAdd(p.n_items + 1, 1);
           item = __shfl_sync(0xffffffffu, item, 0);
+#ifdef SVG2_CTA_TIMES
+          if (lane == 0 && item < n_items) g_cta_times[blockIdx.x][2] += 1;
+#endif
           it = item < n_items ? __ldg(p.items + item) : make_int4(-1, 0, 0, 0);
           mbar_wait(&bars.item_empty[islot], iph ^ 1);
           if (lane == 0) {
@@ -647,6 +661,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef SVG2_CTA_TIMES
+  if (threadIdx.x == 0) g_cta_times[blockIdx.x][1] = globaltimer_ns();
+#endif
   if (warp == kWarpTmem) tmem_dealloc<512>(tmem);
 }
 
@@ -1008,6 +1025,11 @@ cudaError_t launch_varblock_attention(const void* Qp, const void* Kp, const void
 
 }  // namespace svg2
 
+#ifdef SVG2_CTA_TIMES
+extern "C" __attribute__((visibility("default"))) int svg2_cta_times_dump(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, svg2::g_cta_times, sizeof(svg2::g_cta_times)));
+}
+#endif
 #ifdef SVG2_TRACE
 // measurement build only: the cycle trace of the last attention launch, [kTrEv][kTrT] clock64 values
 extern "C" __attribute__((visibility("default"))) int svg2_trace_dump(long long* out) {
