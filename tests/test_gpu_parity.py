@@ -269,6 +269,24 @@ def test_select_topp_diffuse_weights(svg2, oracle_mod, p, Cq, Ck):
             assert pairs_h[0, h] == opairs
 
 
+@pytest.mark.parametrize("Ck,spread", [(700, 0.05), (1500, 2.0), (1500, 0.05), (4000, 2.0), (4000, 0.05)])
+def test_select_topp_repeatable(svg2, Ck, spread):
+    """The threshold search synchronises a team of warps per row through shared memory (team sums, list compaction,
+    narrowing); repeated calls must give the same masks and pair counts bit for bit (a race would show as a
+    nondeterministic boundary).  compute-sanitizer is not available on the test pool, so this is the race check."""
+    rng = np.random.default_rng(Ck)
+    d, Cq = 128, 13
+    cq = torch.from_numpy((rng.standard_normal((1, 3, Cq, d)) * spread).astype(np.float32)).cuda()
+    ck = torch.from_numpy((rng.standard_normal((1, 3, Ck, d)) * spread).astype(np.float32)).cuda()
+    sq = torch.from_numpy(rng.integers(1, 50, (1, 3, Cq)).astype(np.int32)).cuda()
+    sk = torch.from_numpy(rng.integers(0, 10, (1, 3, Ck)).astype(np.int32)).cuda()
+    sk[..., 0] = 3
+    m0, p0 = svg2.select_topp(cq, ck, sq, sk, 0.9)
+    for _ in range(20):
+        m, p = svg2.select_topp(cq, ck, sq, sk, 0.9)
+        assert torch.equal(m, m0) and torch.equal(p, p0)
+
+
 @pytest.mark.parametrize("Ck", [64, 700, 1500, 3000])
 def test_select_topp_exact_ties_follow_j(svg2, oracle_mod, Ck):
     """Equal weights at the top-p boundary (key clusters in groups of 4 with identical centroids and sizes): the sorted
