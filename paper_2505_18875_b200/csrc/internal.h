@@ -7,7 +7,7 @@
 namespace svg2 {
 
 constexpr int kSortTile = 2048;      // labels per histogram / stable-scatter tile
-constexpr int kMaxClusters = 4096;   // C limit (select_topp sorts a row of Ck in shared memory)
+constexpr int kMaxClusters = 4096;   // C limit (a select_topp row of Ck weights lives in one CTA)
 constexpr int kQTile = 128;          // query rows per tcgen05 M=128 tile
 constexpr int kKTile = 128;          // keys per S tile (N of the QK^T MMA, K of the PV MMA)
 constexpr int kItemRows = 2 * kQTile;  // one attention work item = two Q tiles of one query cluster

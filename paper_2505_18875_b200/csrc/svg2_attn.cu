@@ -883,10 +883,24 @@ __global__ void __launch_bounds__(1024) k_parts(const int32_t* __restrict__ q_of
     }
     P += c[u];
   }
+  // the work-list order of this head's clusters: longest key stream first (ties: lower index), k_items lists the
+  // items in this order so the persistent attention launch ends on short items
+  __shared__ int ng_s[kMaxClusters];
+  const int32_t* ng = ws.ngroups + size_t(bh) * Cq;
+  for (int i = tid; i < Cq; i += 1024) ng_s[i] = ng[i];
+  __syncthreads();
+  for (int i = tid; i < Cq; i += 1024) {
+    const int gi = ng_s[i];
+    int rank = 0;
+    for (int k = 0; k < Cq; ++k) {
+      const int gk = ng_s[k];
+      rank += (gk > gi || (gk == gi && k < i)) ? 1 : 0;
+    }
+    ws.order[size_t(bh) * Cq + rank] = i;
+  }
 }
 
-constexpr int kOrderMaxCq = 512;
-// Work items in (b,h)-major order, clusters of a head longest key stream first: ceil(|Q_i| / 256) pairs of 128-row Q
+// Work items in (b,h)-major order, clusters of a head in k_parts' order (longest key stream first): ceil(|Q_i| / 256) pairs of 128-row Q
 // tiles per non-empty query cluster with a non-empty key stream.  One CTA scans all B*H*Cq clusters; also resets the dynamic-scheduler counter.  A
 // query cluster whose mask row selects no non-empty key cluster (a contract violation of svg2_varblock_attention,
 // include/svg2.h; impossible in the fused call, where every row selects >= 1 non-empty cluster) gets no item: its
@@ -899,23 +913,6 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) n_orphan = 0;
   const int total_clusters = BH * Cq;
-  // Within each head the clusters are listed longest key stream first (ties: lower index), so the launch ends on
-  // short items and the persistent CTAs finish together; heads stay in order (their K'/V' stay in L2 one head at a
-  // time).  O(Cq^2) per head: only for Cq <= kOrderMaxCq, else index order.
-  for (int c = tid; c < total_clusters; c += 1024) {
-    const int bh = c / Cq, i = c - bh * Cq;
-    int rank = i;
-    if (Cq <= kOrderMaxCq) {
-      const int32_t* ng = ws.ngroups + size_t(bh) * Cq;
-      const int gi = ng[i];
-      rank = 0;
-      for (int k = 0; k < Cq; ++k) {
-        const int gk = ng[k];
-        rank += (gk > gi || (gk == gi && k < i)) ? 1 : 0;
-      }
-    }
-    ws.order[size_t(bh) * Cq + rank] = i;
-  }
   __syncthreads();
   int base = 0;
   for (int c0 = 0; c0 < total_clusters; c0 += 1024) {
@@ -923,7 +920,7 @@ __global__ void __launch_bounds__(1024) k_items(const int32_t* __restrict__ q_of
     int n = 0, q0 = 0, sq = 0, bh = 0;
     if (c < total_clusters) {
       bh = c / Cq;
-      c = bh * Cq + ws.order[c];  // the cluster at this position of the head's order
+      c = bh * Cq + ws.order[c];  // the cluster at this position of the head's order (k_parts)
       const int i = c - bh * Cq;
       q0 = q_off[size_t(bh) * (Cq + 1) + i];
       sq = q_off[size_t(bh) * (Cq + 1) + i + 1] - q0;
