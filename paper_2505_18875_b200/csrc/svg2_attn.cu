@@ -16,7 +16,9 @@
 // softmax round trip, sets the pace.  Budget (512 TMEM columns): S_a, S_b (kN fp32 each), P_a, P_b (kN/2 packed
 // bf16), O_a, O_b (D fp32), hence kN = 80 keys per tile for d = 128 and 128 for d = 64.
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter):
+// Warp roles (384 threads, 1 CTA per SM, persistent; items fetched dynamically with an atomic counter, in the work-list
+// order k_parts / k_items build: heads in order, each head's query clusters longest key stream first, so the launch
+// ends on short items and the long streams of a head, which share most key clusters, run together in L2):
 //   warps 0-3   softmax warpgroup of Q tile a; warps 4-7 of Q tile b.  One thread = one query row = one TMEM lane
 //               (warp w owns lanes 32(w%4)..+31): tcgen05.ld S, release S, online softmax in registers (exp2 domain,
 //               lazy rescale of O in TMEM when the running max grows by > 8, after the previous PV completed), P
