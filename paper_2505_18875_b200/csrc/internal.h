@@ -177,8 +177,10 @@ cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const 
 cudaError_t launch_scatter_rows(const void* Op, const int32_t* perm, int BH, int N, int d, void* O, cudaStream_t s);
 // FP8 PV: per-(head, channel) |x| max (amax [BH, d], f32 bits) and the gather of X[perm] rounded to e4m3 with channel
 // scales 448 / amax_c
-cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq, uint32_t* amax,
-                                    cudaStream_t s);
+// FP8 PV (R26): per-(b,h,channel) max |V| into amax (zeroed here), then V' = V[perm] in e4m3 with channel scales
+cudaError_t launch_absmax(int BH, int N, int d, XView X, uint32_t* amax, cudaStream_t s);
+cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq,
+                                    const uint32_t* amax, cudaStream_t s);
 // k-means cold-start options (DESIGN R2, R25): strided rows, or k-means++ with the R25 generator
 struct KmeansInit {
   bool kmeanspp = false;

@@ -201,6 +201,12 @@ cudaError_t run_fused(const XView& Q, const XView& K, const XView& V, const svg2
   if (e == cudaSuccess)
     e = launch_kmeans(Q, BH, dm.Nq, dm.d, cfg->Cq, cfg->iters, warm, q_centroids, w.lab_q, w.size_q, w.perm_q,
                       w.off_q, w.km_q, s, nullptr, init_q, gq, dbg ? dbg->q_objective : nullptr);
+  // FP8 PV: the |V| channel maxima depend on V alone, so they run on the Q-role stream while the (longer) K role is
+  // still clustering; only the e4m3 gather through pi_k waits for the join
+  if (e == cudaSuccess && fp8) {
+    if (arrive) cudaStreamWaitEvent(s, arrive[2], 0);
+    e = launch_absmax(BH, dm.Nk, dm.d, V, w.v_amax, s);
+  }
   if (s2) {  // join (always, so no work is left behind on s2 even after an error) and release (deferred by CUDA)
     cudaEventRecord(ev_join, s2);
     cudaStreamWaitEvent(s, ev_join, 0);

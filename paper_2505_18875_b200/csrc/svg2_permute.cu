@@ -280,8 +280,7 @@ cudaError_t launch_gather_rows(const int32_t* perm, int BH, int N, int d, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq, uint32_t* amax,
-                                    cudaStream_t s) {
+cudaError_t launch_absmax(int BH, int N, int d, XView X, uint32_t* amax, cudaStream_t s) {
   const int vpr = d / 8;
   cudaMemsetAsync(amax, 0, size_t(BH) * d * sizeof(uint32_t), s);
   int dev = 0, sms = 148;
@@ -290,6 +289,17 @@ cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, X
   const int per_bh = (sms * 8 + BH - 1) / BH;
   const int lg = 31 - __builtin_clz(unsigned(vpr));  // d / 8 = 8 or 16
   k_absmax<<<dim3(per_bh, BH), 256, 0, s>>>(X, N * vpr, lg, amax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows_e4m3(const int32_t* perm, int BH, int N, int d, XView X, void* Xq,
+                                    const uint32_t* amax, cudaStream_t s) {
+  const int vpr = d / 8;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_bh = (sms * 8 + BH - 1) / BH;
+  const int lg = 31 - __builtin_clz(unsigned(vpr));
   k_gather_rows_e4m3<<<dim3(per_bh, BH), 256, 0, s>>>(perm, N, lg, X, static_cast<uint2*>(Xq), amax);
   return cudaGetLastError();
 }
