@@ -150,9 +150,10 @@ __device__ __forceinline__ int team_excl_scan(int v, int* total, long long (*red
 //   2) top-p without sorting (R27): with B(v) = sum of the w >= v, the ranks the sorted walk selects (mass before
 //      the rank < p Z) are exactly the w >= w*, w* = max{v : B(v) >= p Z} -- the first rank whose inclusive mass
 //      reaches p Z.  B is monotone in v and positive doubles order like their bit patterns, so w* is found bit by
-//      bit from the top (63 team sums of the thread-local partial masses).  Entries equal to w* (only equal
-//      centroids and sizes give such ties) are then ordered by ascending j as the sort would: the k-th of them is
-//      selected iff B(> w*) + k w* < p Z.
+//      bit from the top: 11 team sums over all entries fix its binade, whose weights are compacted into shared memory
+//      and narrowed 8 bits per level while more than kShortList remain; a short list is resolved directly (see the
+//      code).  Entries equal to w* (only equal centroids and sizes give such ties) are then ordered by ascending j as
+//      the sort would: the k-th of them is selected iff B(> w*) + k w* < p Z.
 template <int E, int R>
 __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ S, const int32_t* __restrict__ sq,
                                                         const int32_t* __restrict__ sk, int Cq, int Ck, double top_p,
